@@ -1,0 +1,156 @@
+/* include/hftw.h -- C ABI of the B200-native minimal-weather timestep.
+ *
+ * This is the drop-in boundary for the reference's native weather simulator
+ * (/root/reference/proj/include/hft/weather.hpp).  Each entry point names the
+ * reference interface it replaces.  Plain pointers and sizes only: no torch,
+ * no C++ types.  Exported from paper_1802_05839_b200/libhftw.so (nvcc, sm_100a).
+ *
+ * Conventions:
+ *  - Every function returns 0 on success, a nonzero HFTW_E* code otherwise;
+ *    hftw_last_error(ctx) (or hftw_last_error(NULL) for create failures)
+ *    returns the message.  No exceptions cross the ABI.
+ *  - Host buffers use the reference's unpadded LOGICAL column-major layout of
+ *    hft::ArrayObject::data (interpreter.hpp:25-36): 3D fields over
+ *    (0..nx+1, 0..ny+1, 1..nz), 2D fields over (0..nx+1, 0..ny+1)
+ *    (weather.cpp:71,77).  One memcpy fills SimState::field.data.  Pinned host
+ *    memory makes transfers run at full PCIe rate but is not required.
+ *  - The library owns device memory, streams, tensor maps and graphs; the
+ *    caller owns host buffers.  One host thread per context.
+ *  - Arithmetic is bitwise identical to hft::reference_step: every kernel
+ *    uses explicitly rounded IEEE double ops (__dadd_rn/__dmul_rn), i.e. no
+ *    FMA contraction, and the reference's association order.
+ */
+#ifndef HFTW_H
+#define HFTW_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HFTW_ABI_VERSION 1
+
+/* Mirrors hft::GridConfig field for field (weather.hpp:26-35). */
+typedef struct hftw_grid {
+    int64_t nx, ny, nz;
+    double timestep;
+    double output_timestep;
+    double diffusion_velocity;
+    double radiation_intensity;
+    double transfer_velocity;
+    double surf_energy;
+    double pbl_energy;
+} hftw_grid;
+
+/* The four SimState members (weather.hpp:39-46). */
+enum hftw_field {
+    HFTW_ENERGY = 0,
+    HFTW_ENERGY_U = 1,
+    HFTW_ENERGY_SURF = 2,
+    HFTW_ENERGY_PBL = 3
+};
+
+/* Device storage order of 3D fields (BuildConfig::storage_order, config.hpp:41-43;
+ * permutation semantics of unpermute_storage, weather.cpp:306-338):
+ *   IJK = {1,2,3}: i fastest (the reference GPU default).
+ *   KIJ = {3,1,2}: raw tuple (k,i,j), k fastest (the paper's CPU-friendly order). */
+enum hftw_layout { HFTW_IJK = 0, HFTW_KIJ = 1 };
+
+/* Step kernel selection (hftw_set_kernel).  AUTO picks the fastest valid one. */
+enum hftw_kernel {
+    HFTW_KERNEL_AUTO = 0,
+    HFTW_KERNEL_FUSED_TMA = 1, /* fused physics+diffusion, TMA row-slab pipeline */
+    HFTW_KERNEL_FUSED_CELL = 2, /* fused physics+diffusion, one cell per thread */
+    HFTW_KERNEL_SPLIT = 3       /* reference structure: physics pass, then diffusion pass */
+};
+
+enum hftw_error {
+    HFTW_OK = 0,
+    HFTW_EINVAL = 1,   /* invalid argument or grid (validate() failed) */
+    HFTW_ECUDA = 2,    /* CUDA runtime/driver error */
+    HFTW_ENOMEM = 3,   /* device allocation failed */
+    HFTW_ESTATE = 4,   /* call not valid in the current context state */
+    HFTW_EUNSUP = 5    /* unsupported combination (e.g. TMA kernel with nz > 256) */
+};
+
+typedef struct hftw_ctx hftw_ctx;
+
+/* ABI version of the loaded library (HFTW_ABI_VERSION). */
+int hftw_abi_version(void);
+
+/* hft::validate (weather.hpp:37, weather.cpp:24-41).  Returns 0 when valid,
+ * HFTW_EINVAL otherwise with the reference's diagnostics, one per line, in
+ * msg (truncated to cap). */
+int hftw_validate(const hftw_grid* grid, char* msg, size_t cap);
+
+/* Create a context for `grid` on CUDA device `device` with the given storage
+ * layout.  Fields are allocated but undefined until hftw_init/hftw_upload. */
+int hftw_create(const hftw_grid* grid, int layout, int device, hftw_ctx** out);
+
+/* Release everything the context owns. NULL is accepted. */
+void hftw_destroy(hftw_ctx* ctx);
+
+/* hft::reference_init (weather.hpp:48-51, weather.cpp:67-99), on the device. */
+int hftw_init(hftw_ctx* ctx);
+
+/* Host -> device copy of one field from its logical column-major buffer. */
+int hftw_upload(hftw_ctx* ctx, int field, const double* host);
+
+/* Device -> host copy of one field into its logical column-major buffer.
+ * Synchronous with respect to the context stream. */
+int hftw_download(hftw_ctx* ctx, int field, double* host);
+
+/* nsteps x hft::reference_step (weather.hpp:53-55, weather.cpp:101-171),
+ * asynchronous on the context stream.  After the call ENERGY holds the new
+ * field and ENERGY_U the post-physics, pre-diffusion field of the last step,
+ * exactly as after the reference's buffer swap (weather.cpp:170). */
+int hftw_step(hftw_ctx* ctx, int64_t nsteps);
+
+/* Wait for all work queued on the context stream. */
+int hftw_sync(hftw_ctx* ctx);
+
+/* Error text of the last failing call (ctx may be NULL). */
+const char* hftw_last_error(const hftw_ctx* ctx);
+
+/* hft::run_reference (weather.hpp:57-59, weather.cpp:173-178) in one call:
+ * create on `device`, init, steps, download the four fields into the caller's
+ * buffers (any may be NULL), destroy. */
+int hftw_run_reference(const hftw_grid* grid, int64_t steps, int device, double* energy,
+                       double* energy_u, double* energy_surf, double* energy_pbl);
+
+/* ---- measurement / configuration hooks (not part of the reference API) ---- */
+
+/* Run the context's work on an external cudaStream_t (NULL = own stream). */
+int hftw_set_stream(hftw_ctx* ctx, void* cuda_stream);
+/* The cudaStream_t kernels are launched on. */
+void* hftw_stream(hftw_ctx* ctx);
+/* Select the step kernel (enum hftw_kernel). */
+int hftw_set_kernel(hftw_ctx* ctx, int kernel);
+/* Kernel actually used by hftw_step (resolves AUTO). */
+int hftw_get_kernel(const hftw_ctx* ctx);
+
+/* Phase 1 alone (weather.cpp:118-128): in-place column physics on ENERGY.
+ * mode 0 = one column per thread with the k loop in registers (the
+ * reference's emitted GPU mapping, emit_cuda.cpp:159-214), 1 = one cell per
+ * thread along the fastest storage dimension.  Leaves ENERGY_U untouched. */
+int hftw_physics(hftw_ctx* ctx, int mode);
+/* Phases 2-5 alone (weather.cpp:130-168): ENERGY <- diffusion(ENERGY), with
+ * ENERGY_U receiving the previous ENERGY (the swap of weather.cpp:170). */
+int hftw_diffuse(hftw_ctx* ctx);
+
+/* Algorithmic HBM bytes of one call: what = 0 full step, 1 physics, 2 diffusion
+ * (16 B per stored cell + 16 B per column for a step). */
+double hftw_algorithmic_bytes(const hftw_ctx* ctx, int what);
+/* Number of kernel launches one hftw_step(ctx, 1) enqueues. */
+int hftw_launches_per_step(const hftw_ctx* ctx);
+
+/* Raw device view of a field for zero-copy interop: base pointer of logical
+ * (i=0, j=0, k=1) and element strides (si, sj, sk); sk = 0 for 2D fields. */
+int hftw_field_view(hftw_ctx* ctx, int field, void** dptr, int64_t strides[3]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HFTW_H */

@@ -1,0 +1,89 @@
+"""ctypes binding of libhftw.so (include/hftw.h).
+
+There is deliberately no fallback: if the CUDA library is missing or no GPU
+is visible, every compute entry point raises.  The binding itself (symbol
+table, struct layout) is usable without a GPU so CPU tests can check the
+exported ABI.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from ._build import LIB
+
+HFTW_ENERGY, HFTW_ENERGY_U, HFTW_ENERGY_SURF, HFTW_ENERGY_PBL = range(4)
+FIELDS = {"energy": HFTW_ENERGY, "energy_u": HFTW_ENERGY_U,
+          "energy_surf": HFTW_ENERGY_SURF, "energy_pbl": HFTW_ENERGY_PBL}
+LAYOUTS = {"ijk": 0, "kij": 1}
+KERNELS = {"auto": 0, "fused_tma": 1, "fused_cell": 2, "split": 3}
+KERNEL_NAMES = {v: k for k, v in KERNELS.items()}
+ERRORS = {0: "ok", 1: "EINVAL", 2: "ECUDA", 3: "ENOMEM", 4: "ESTATE", 5: "EUNSUP"}
+
+
+class hftw_grid(C.Structure):
+    """Mirror of hft::GridConfig (weather.hpp:26-35) / hftw_grid (include/hftw.h)."""
+
+    _fields_ = [("nx", C.c_int64), ("ny", C.c_int64), ("nz", C.c_int64),
+                ("timestep", C.c_double), ("output_timestep", C.c_double),
+                ("diffusion_velocity", C.c_double), ("radiation_intensity", C.c_double),
+                ("transfer_velocity", C.c_double), ("surf_energy", C.c_double),
+                ("pbl_energy", C.c_double)]
+
+
+class HftwError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"hftw error {ERRORS.get(code, code)}: {msg}")
+        self.code = code
+
+
+# (name, restype, argtypes) for every symbol include/hftw.h declares
+_P = C.c_void_p
+_D = C.POINTER(C.c_double)
+SIGNATURES = [
+    ("hftw_abi_version", C.c_int, []),
+    ("hftw_validate", C.c_int, [C.POINTER(hftw_grid), C.c_char_p, C.c_size_t]),
+    ("hftw_create", C.c_int, [C.POINTER(hftw_grid), C.c_int, C.c_int, C.POINTER(_P)]),
+    ("hftw_destroy", None, [_P]),
+    ("hftw_init", C.c_int, [_P]),
+    ("hftw_upload", C.c_int, [_P, C.c_int, _D]),
+    ("hftw_download", C.c_int, [_P, C.c_int, _D]),
+    ("hftw_step", C.c_int, [_P, C.c_int64]),
+    ("hftw_sync", C.c_int, [_P]),
+    ("hftw_last_error", C.c_char_p, [_P]),
+    ("hftw_run_reference", C.c_int, [C.POINTER(hftw_grid), C.c_int64, C.c_int, _D, _D, _D, _D]),
+    ("hftw_set_stream", C.c_int, [_P, _P]),
+    ("hftw_stream", _P, [_P]),
+    ("hftw_set_kernel", C.c_int, [_P, C.c_int]),
+    ("hftw_get_kernel", C.c_int, [_P]),
+    ("hftw_physics", C.c_int, [_P, C.c_int]),
+    ("hftw_diffuse", C.c_int, [_P]),
+    ("hftw_algorithmic_bytes", C.c_double, [_P, C.c_int]),
+    ("hftw_launches_per_step", C.c_int, [_P]),
+    ("hftw_field_view", C.c_int, [_P, C.c_int, C.POINTER(_P), C.POINTER(C.c_int64)]),
+]
+
+_lib = None
+
+
+def lib(path: str = LIB) -> C.CDLL:
+    """Load libhftw.so (building it first when absent and nvcc exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        from ._build import build
+        build()
+    L = C.CDLL(path)
+    for name, res, args in SIGNATURES:
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+def check(rc: int, ctx=None) -> None:
+    if rc != 0:
+        msg = lib().hftw_last_error(ctx)
+        raise HftwError(rc, msg.decode() if msg else "")

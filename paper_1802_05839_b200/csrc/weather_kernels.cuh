@@ -1,0 +1,493 @@
+// weather_kernels.cuh -- sm_100a kernels of the minimal-weather timestep.
+//
+// Reference hot path: hft::reference_step, /root/reference/proj/src/weather.cpp:101-171
+//   (1) column physics in place            weather.cpp:118-128
+//   (2) inner diffusion                    weather.cpp:130-137
+//   (3) k = 1 / k = nz planes              weather.cpp:139-150
+//   (4) j ghost rows (cyclic)              weather.cpp:152-159
+//   (5) i ghost columns (cyclic, corners)  weather.cpp:161-168
+//   (6) buffer swap                        weather.cpp:170
+//
+// Bitwise parity: every arithmetic operation is an explicitly rounded IEEE
+// double op (__dadd_rn/__dsub_rn/__dmul_rn), which nvcc never contracts into
+// DFMA, in exactly the reference's order and association.  Coefficients
+// (1 - c*dv) are computed on the host the way the reference computes them.
+//
+// Fused formulation (SURVEY.md 8(a) "Fused-step specification"): the new
+// value of a cell needs the post-physics value P of itself and of its
+// neighbours; P is pointwise given sf/pb, so every kernel reads the
+// pre-physics field e once and recomputes P on the fly.  The post-physics
+// field (SimState::energy_u) is materialised only when somebody asks for it.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hftw {
+
+// Device-side description of one (sub)domain.  Logical indices follow the
+// reference: i in [0, nx+1], j in [0, ny+1], k in [1, nz]; the pointers
+// passed to the kernels already point at logical (0, 0, 1) (3D) or (0, 0)
+// (2D), and slots i = -1, nx+2 / j = -1, ny+2 exist (halo slots for the
+// decomposed run; unused on one GPU).
+struct Dom {
+    int nx, ny, nz;       // (local) interior extents
+    long long si, sj, sk; // 3D element strides
+    long long s2j;        // 2D row stride (2D i-stride is 1)
+    int own_w, own_e, own_s, own_n; // this domain owns the global ghost column/row
+    int wfar, efar, sfar, nfar;     // index holding the cyclic partner of a ghost cell
+    double ri, tv, dv;    // radiation_intensity, transfer_velocity, diffusion_velocity
+    double c2, c5, c6;    // (1 - 2.0*dv), (1 - 5.0*dv), (1 - 6.0*dv) as in weather.cpp
+};
+
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+
+// Post-physics value of one cell, weather.cpp:122-127:
+//   e = e + ri;  k==1: e = e - tv*(e - sf);  k==nz: e = e - tv*(e - pb).
+template <bool PHYS>
+__device__ __forceinline__ double phys(double ev, int k, int nz, double sfv, double pbv,
+                                       double ri, double tv) {
+    if (!PHYS) return ev;
+    double p = dadd(ev, ri);
+    if (k == 1) p = dsub(p, dmul(tv, dsub(p, sfv)));
+    if (k == nz) p = dsub(p, dmul(tv, dsub(p, pbv)));
+    return p;
+}
+
+template <bool PHYS>
+__device__ __forceinline__ double P_at(const double* __restrict__ e,
+                                       const double* __restrict__ sf,
+                                       const double* __restrict__ pb, const Dom& d, int i, int j,
+                                       int k) {
+    double ev = __ldg(e + i * d.si + j * d.sj + (long long)(k - 1) * d.sk);
+    double sfv = 0.0, pbv = 0.0;
+    if (PHYS && k == 1) sfv = __ldg(sf + i + j * d.s2j);
+    if (PHYS && k == d.nz) pbv = __ldg(pb + i + j * d.s2j);
+    return phys<PHYS>(ev, k, d.nz, sfv, pbv, d.ri, d.tv);
+}
+
+// New value of one owned cell, in the reference's region precedence
+// (i ghosts win over j ghosts, which win over the k planes).
+template <bool PHYS>
+__device__ __forceinline__ double cell_update(const double* __restrict__ e,
+                                              const double* __restrict__ sf,
+                                              const double* __restrict__ pb, const Dom& d, int i,
+                                              int j, int k) {
+    if ((d.own_w && i == 0) || (d.own_e && i == d.nx + 1)) {
+        // weather.cpp:164-167: (1-2dv)*e(i) + dv*(e(1) + e(nx))
+        double a = P_at<PHYS>(e, sf, pb, d, i == 0 ? 1 : d.efar, j, k);
+        double b = P_at<PHYS>(e, sf, pb, d, i == 0 ? d.wfar : d.nx, j, k);
+        return dadd(dmul(d.c2, P_at<PHYS>(e, sf, pb, d, i, j, k)), dmul(d.dv, dadd(a, b)));
+    }
+    if ((d.own_s && j == 0) || (d.own_n && j == d.ny + 1)) {
+        // weather.cpp:155-158: (1-2dv)*e(j) + dv*(e(ny) + e(1))
+        double a = P_at<PHYS>(e, sf, pb, d, i, j == 0 ? d.sfar : d.ny, k);
+        double b = P_at<PHYS>(e, sf, pb, d, i, j == 0 ? 1 : d.nfar, k);
+        return dadd(dmul(d.c2, P_at<PHYS>(e, sf, pb, d, i, j, k)), dmul(d.dv, dadd(a, b)));
+    }
+    double c = P_at<PHYS>(e, sf, pb, d, i, j, k);
+    double s = dadd(P_at<PHYS>(e, sf, pb, d, i - 1, j, k), P_at<PHYS>(e, sf, pb, d, i + 1, j, k));
+    s = dadd(s, P_at<PHYS>(e, sf, pb, d, i, j - 1, k));
+    s = dadd(s, P_at<PHYS>(e, sf, pb, d, i, j + 1, k));
+    if (k == 1) { // weather.cpp:142-145
+        s = dadd(s, P_at<PHYS>(e, sf, pb, d, i, j, 2));
+        return dadd(dmul(d.c5, c), dmul(d.dv, s));
+    }
+    if (k == d.nz) { // weather.cpp:146-149
+        s = dadd(s, P_at<PHYS>(e, sf, pb, d, i, j, d.nz - 1));
+        return dadd(dmul(d.c5, c), dmul(d.dv, s));
+    }
+    // weather.cpp:134-137
+    s = dadd(s, P_at<PHYS>(e, sf, pb, d, i, j, k - 1));
+    s = dadd(s, P_at<PHYS>(e, sf, pb, d, i, j, k + 1));
+    return dadd(dmul(d.c6, c), dmul(d.dv, s));
+}
+
+// Owned index ranges of a domain.
+struct Owned {
+    int i0, i1, j0, j1;
+};
+__device__ __forceinline__ Owned owned(const Dom& d) {
+    return {d.own_w ? 0 : 1, d.own_e ? d.nx + 1 : d.nx, d.own_s ? 0 : 1,
+            d.own_n ? d.ny + 1 : d.ny};
+}
+
+//------------------------------------------------------------------------------
+// FUSED_CELL: one owned cell per thread, fastest storage dimension first.
+// Valid for every layout; the generic path and the correctness baseline.
+//------------------------------------------------------------------------------
+template <bool KFAST, bool PHYS>
+__global__ void __launch_bounds__(256) step_cell_kernel(const double* __restrict__ e,
+                                                        double* __restrict__ u,
+                                                        const double* __restrict__ sf,
+                                                        const double* __restrict__ pb, Dom d) {
+    Owned o = owned(d);
+    const long long ni = o.i1 - o.i0 + 1, nj = o.j1 - o.j0 + 1, nk = d.nz;
+    const long long n = ni * nj * nk;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+         t += (long long)gridDim.x * blockDim.x) {
+        int i, j, k;
+        if (KFAST) {
+            k = 1 + (int)(t % nk);
+            long long r = t / nk;
+            i = o.i0 + (int)(r % ni);
+            j = o.j0 + (int)(r / ni);
+        } else {
+            i = o.i0 + (int)(t % ni);
+            long long r = t / ni;
+            j = o.j0 + (int)(r % nj);
+            k = 1 + (int)(r / nj);
+        }
+        u[i * d.si + j * d.sj + (long long)(k - 1) * d.sk] = cell_update<PHYS>(e, sf, pb, d, i, j, k);
+    }
+}
+
+//------------------------------------------------------------------------------
+// Column physics alone, in place (weather.cpp:118-128).
+//  COLUMN: one (i,j) column per thread, k loop in registers -- the
+//          reference's emitted GPU mapping (hfk0_radiate + exchange,
+//          emit_cuda.cpp:159-214).  Coalesced in IJK, strided in KIJ.
+//  cell:   one cell per thread along the fastest storage dimension.
+//------------------------------------------------------------------------------
+template <bool COLUMN, bool KFAST>
+__global__ void __launch_bounds__(256) physics_kernel(double* __restrict__ e,
+                                                      const double* __restrict__ sf,
+                                                      const double* __restrict__ pb, Dom d) {
+    Owned o = owned(d);
+    const long long ni = o.i1 - o.i0 + 1, nj = o.j1 - o.j0 + 1;
+    if (COLUMN) {
+        const long long n = ni * nj;
+        for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+             t += (long long)gridDim.x * blockDim.x) {
+            int i = o.i0 + (int)(t % ni), j = o.j0 + (int)(t / ni);
+            double* col = e + i * d.si + j * d.sj;
+            for (int k = 1; k <= d.nz; ++k) {
+                double* p = col + (long long)(k - 1) * d.sk;
+                *p = dadd(*p, d.ri);
+            }
+            double s = __ldg(sf + i + j * d.s2j), b = __ldg(pb + i + j * d.s2j);
+            double v = col[0];
+            col[0] = dsub(v, dmul(d.tv, dsub(v, s)));
+            double* top = col + (long long)(d.nz - 1) * d.sk;
+            v = *top;
+            *top = dsub(v, dmul(d.tv, dsub(v, b)));
+        }
+    } else {
+        const long long nk = d.nz, n = ni * nj * nk;
+        for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+             t += (long long)gridDim.x * blockDim.x) {
+            int i, j, k;
+            if (KFAST) {
+                k = 1 + (int)(t % nk);
+                long long r = t / nk;
+                i = o.i0 + (int)(r % ni);
+                j = o.j0 + (int)(r / ni);
+            } else {
+                i = o.i0 + (int)(t % ni);
+                long long r = t / ni;
+                j = o.j0 + (int)(r % nj);
+                k = 1 + (int)(r / nj);
+            }
+            double* p = e + i * d.si + j * d.sj + (long long)(k - 1) * d.sk;
+            double sfv = 0.0, pbv = 0.0;
+            if (k == 1) sfv = __ldg(sf + i + j * d.s2j);
+            if (k == d.nz) pbv = __ldg(pb + i + j * d.s2j);
+            *p = phys<true>(*p, k, d.nz, sfv, pbv, d.ri, d.tv);
+        }
+    }
+}
+
+//------------------------------------------------------------------------------
+// Device-side reference_init (weather.cpp:86-98): 300 inside the integer box
+// [n/4, 3n/4] of every dimension, 0 elsewhere (buffers pre-zeroed); surface
+// and boundary-layer constants over all columns.
+//------------------------------------------------------------------------------
+template <bool KFAST>
+__global__ void init_kernel(double* __restrict__ e, double* __restrict__ sf,
+                            double* __restrict__ pb, Dom d, int gnx, int gny, int gnz, int gi0,
+                            int gj0, double surf, double pbl) {
+    Owned o = owned(d);
+    const long long ni = o.i1 - o.i0 + 1, nj = o.j1 - o.j0 + 1, nk = d.nz;
+    const long long n = ni * nj * nk;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+         t += (long long)gridDim.x * blockDim.x) {
+        int i, j, k;
+        if (KFAST) {
+            k = 1 + (int)(t % nk);
+            long long r = t / nk;
+            i = o.i0 + (int)(r % ni);
+            j = o.j0 + (int)(r / ni);
+        } else {
+            i = o.i0 + (int)(t % ni);
+            long long r = t / ni;
+            j = o.j0 + (int)(r % nj);
+            k = 1 + (int)(r / nj);
+        }
+        const long long gi = gi0 + i, gj = gj0 + j; // global logical indices
+        const bool in = gi >= gnx / 4 && gi <= (3LL * gnx) / 4 && gj >= gny / 4 &&
+                        gj <= (3LL * gny) / 4 && k >= gnz / 4 && k <= (3LL * gnz) / 4;
+        e[i * d.si + j * d.sj + (long long)(k - 1) * d.sk] = in ? 300.0 : 0.0;
+        if (k == 1) {
+            sf[i + j * d.s2j] = surf;
+            pb[i + j * d.s2j] = pbl;
+        }
+    }
+}
+
+// Logical column-major dense <-> strided device layout (upload/download of
+// the KIJ store).  One thread per logical element in logical order, so the
+// dense side is coalesced.
+template <bool TO_STRIDED>
+__global__ void relayout_kernel(const double* __restrict__ src, double* __restrict__ dst,
+                                long long ni, long long nj, long long nk, long long si,
+                                long long sj, long long sk) {
+    const long long n = ni * nj * nk;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+         t += (long long)gridDim.x * blockDim.x) {
+        long long i = t % ni, r = t / ni, j = r % nj, k = r / nj;
+        long long off = i * si + j * sj + k * sk;
+        if (TO_STRIDED) dst[off] = src[t];
+        else dst[t] = src[off];
+    }
+}
+
+//------------------------------------------------------------------------------
+// FUSED_TMA: the roofline kernel for the IJK store.
+//
+// Work decomposition: the interior (i in 1..nx, j in 1..ny) is cut into
+// i-strips of TX cells; a CTA owns a contiguous range of (strip, row) pairs and
+// marches along j.  For every row it streams one SLAB -- the (TX+2) x nz
+// block {i0-1 .. i0+TX} x {j} x {1..nz} -- into shared memory with ONE 3D TMA
+// load (box {TX+2, 1, nz}), plus the matching sf/pb rows.  Row j is computed
+// from slabs j-1, j, j+1 held in an NS-deep mbarrier ring, so each e value
+// crosses HBM once (plus a 2/TX halo share that L2 serves) and u is written
+// once with 256-byte aligned coalesced stores.  The k direction needs no halo
+// at all: the whole column is in the slab.
+//
+// Warp roles: NCW consumer warps compute; one producer warp issues the TMA
+// loads.  Ghost cells (regions 4 and 5 of the reference, 0.3% of cells at
+// ASUCA size) are computed by the consumers from global memory in the
+// prologue while the first slabs are in flight.
+//------------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "HFTW_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra HFTW_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Shared-memory geometry of one pipeline stage.
+struct SlabGeom {
+    int w;          // TX + 2 doubles per slab row
+    int e_bytes;    // slab bytes rounded to 128
+    int r_bytes;    // one sf/pb row rounded to 128
+    int stage;      // e + sf + pb
+    int tx_bytes;   // bytes the TMA actually delivers per stage
+};
+__host__ __device__ inline SlabGeom slab_geom(int tx, int nz) {
+    SlabGeom g;
+    g.w = tx + 2;
+    g.e_bytes = ((g.w * nz * 8) + 127) / 128 * 128;
+    g.r_bytes = ((g.w * 8) + 127) / 128 * 128;
+    g.stage = g.e_bytes + 2 * g.r_bytes;
+    g.tx_bytes = g.w * nz * 8 + 2 * g.w * 8;
+    return g;
+}
+
+struct TmaArgs {
+    int fp;       // tensor-map i coordinate of logical i = 0
+    int jrow0;    // tensor-map row coordinate of logical j = 0
+    int nstrips;
+    int ns;       // pipeline depth
+    long long ghost_cells;
+};
+
+template <int TX, int NCW, bool PHYS>
+__global__ void __launch_bounds__((NCW + 1) * 32, 1)
+    step_tma_kernel(const __grid_constant__ CUtensorMap tm_e,
+                    const __grid_constant__ CUtensorMap tm_sf,
+                    const __grid_constant__ CUtensorMap tm_pb, const double* __restrict__ e,
+                    double* __restrict__ u, const double* __restrict__ sf,
+                    const double* __restrict__ pb, Dom d, TmaArgs a,
+                    const int2* __restrict__ ranges) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    const SlabGeom G = slab_geom(TX, d.nz);
+    const int NS = a.ns;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NS * G.stage);
+    uint64_t* empty = full + NS;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int2 rg = ranges[blockIdx.x]; // [begin, end) over linear rows s*ny + (j-1)
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NCW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == NCW) {
+        // ---------------- producer warp ----------------
+        if (lane == 0) {
+            uint32_t L = 0;
+            int r = rg.x;
+            while (r < rg.y) {
+                const int s = r / d.ny, ja = r % d.ny + 1;
+                const int jb = min(d.ny, ja + (rg.y - r) - 1);
+                const int ic = a.fp + 1 + s * TX - 1; // tensor coordinate of i0 - 1
+                for (int jj = ja - 1; jj <= jb + 1; ++jj, ++L) {
+                    const uint32_t slot = L % NS;
+                    if (L >= (uint32_t)NS) mbar_wait(&empty[slot], ((L / NS) - 1) & 1);
+                    unsigned char* st = smem + (size_t)slot * G.stage;
+                    mbar_expect_tx(&full[slot], G.tx_bytes);
+                    tma_load_3d(st, &tm_e, &full[slot], ic, a.jrow0 + jj, 0);
+                    tma_load_2d(st + G.e_bytes, &tm_sf, &full[slot], ic, a.jrow0 + jj);
+                    tma_load_2d(st + G.e_bytes + G.r_bytes, &tm_pb, &full[slot], ic,
+                                a.jrow0 + jj);
+                }
+                r += jb - ja + 1;
+            }
+        }
+        return;
+    }
+
+    // ---------------- consumer warps ----------------
+    // Prologue: this CTA's share of the ghost cells, straight from global.
+    {
+        Owned o = owned(d);
+        const long long nrow = (long long)d.nx * d.nz; // one j-ghost row, i in 1..nx
+        const long long njg = (long long)(d.own_s + d.own_n) * nrow;
+        const long long ncol = (long long)(o.j1 - o.j0 + 1) * d.nz;
+        const long long tid = (long long)blockIdx.x * (NCW * 32) + threadIdx.x;
+        for (long long g = tid; g < a.ghost_cells; g += (long long)gridDim.x * (NCW * 32)) {
+            int i, j, k;
+            if (g < njg) {
+                const long long which = g / nrow, rem = g % nrow;
+                i = 1 + (int)(rem % d.nx);
+                k = 1 + (int)(rem / d.nx);
+                j = (which == 0 && d.own_s) ? 0 : d.ny + 1;
+            } else {
+                const long long h = g - njg, which = h / ncol, rem = h % ncol;
+                j = o.j0 + (int)(rem % (o.j1 - o.j0 + 1));
+                k = 1 + (int)(rem / (o.j1 - o.j0 + 1));
+                i = (which == 0 && d.own_w) ? 0 : d.nx + 1;
+            }
+            u[i * d.si + j * d.sj + (long long)(k - 1) * d.sk] =
+                cell_update<PHYS>(e, sf, pb, d, i, j, k);
+        }
+    }
+
+    constexpr int HALVES = TX / 32;
+    const int items = d.nz * HALVES;
+    uint32_t L = 0; // load index of slab (j - 1) for the current row
+    int r = rg.x;
+    while (r < rg.y) {
+        const int s = r / d.ny, ja = r % d.ny + 1;
+        const int jb = min(d.ny, ja + (rg.y - r) - 1);
+        const int i0 = 1 + s * TX;
+        const int width = min(TX, d.nx - i0 + 1);
+        for (int j = ja; j <= jb; ++j, ++L) {
+            const uint32_t l0 = L, l1 = L + 1, l2 = L + 2;
+            if (j == ja) {
+                mbar_wait(&full[l0 % NS], (l0 / NS) & 1);
+                mbar_wait(&full[l1 % NS], (l1 / NS) & 1);
+            }
+            mbar_wait(&full[l2 % NS], (l2 / NS) & 1);
+            const unsigned char* stm = smem + (size_t)(l0 % NS) * G.stage;
+            const unsigned char* st0 = smem + (size_t)(l1 % NS) * G.stage;
+            const unsigned char* stp = smem + (size_t)(l2 % NS) * G.stage;
+            const double* Em = reinterpret_cast<const double*>(stm);
+            const double* E0 = reinterpret_cast<const double*>(st0);
+            const double* Ep = reinterpret_cast<const double*>(stp);
+            const double* Sm = reinterpret_cast<const double*>(stm + G.e_bytes);
+            const double* S0 = reinterpret_cast<const double*>(st0 + G.e_bytes);
+            const double* Sp = reinterpret_cast<const double*>(stp + G.e_bytes);
+            const double* Bm = reinterpret_cast<const double*>(stm + G.e_bytes + G.r_bytes);
+            const double* B0 = reinterpret_cast<const double*>(st0 + G.e_bytes + G.r_bytes);
+            const double* Bp = reinterpret_cast<const double*>(stp + G.e_bytes + G.r_bytes);
+            double* urow = u + (long long)(i0 - 1) * d.si + (long long)j * d.sj;
+            for (int it = warp; it < items; it += NCW) {
+                const int k = it / HALVES + 1;
+                const int ii = 1 + (it % HALVES) * 32 + lane; // slab column; 0 is i0-1
+                if (ii > width) continue;
+                const int o = (k - 1) * G.w + ii;
+                double c, s6;
+                if (!PHYS || (k != 1 && k != d.nz)) {
+                    c = phys<PHYS>(E0[o], k, d.nz, 0.0, 0.0, d.ri, d.tv);
+                    s6 = dadd(phys<PHYS>(E0[o - 1], k, d.nz, 0.0, 0.0, d.ri, d.tv),
+                              phys<PHYS>(E0[o + 1], k, d.nz, 0.0, 0.0, d.ri, d.tv));
+                    s6 = dadd(s6, phys<PHYS>(Em[o], k, d.nz, 0.0, 0.0, d.ri, d.tv));
+                    s6 = dadd(s6, phys<PHYS>(Ep[o], k, d.nz, 0.0, 0.0, d.ri, d.tv));
+                } else {
+                    c = phys<PHYS>(E0[o], k, d.nz, S0[ii], B0[ii], d.ri, d.tv);
+                    s6 = dadd(phys<PHYS>(E0[o - 1], k, d.nz, S0[ii - 1], B0[ii - 1], d.ri, d.tv),
+                              phys<PHYS>(E0[o + 1], k, d.nz, S0[ii + 1], B0[ii + 1], d.ri, d.tv));
+                    s6 = dadd(s6, phys<PHYS>(Em[o], k, d.nz, Sm[ii], Bm[ii], d.ri, d.tv));
+                    s6 = dadd(s6, phys<PHYS>(Ep[o], k, d.nz, Sp[ii], Bp[ii], d.ri, d.tv));
+                }
+                double out;
+                if (k == 1 || k == d.nz) {
+                    const int kk = k == 1 ? 2 : d.nz - 1;
+                    const int ok = (kk - 1) * G.w + ii;
+                    s6 = dadd(s6, phys<PHYS>(E0[ok], kk, d.nz, S0[ii], B0[ii], d.ri, d.tv));
+                    out = dadd(dmul(d.c5, c), dmul(d.dv, s6));
+                } else {
+                    const double dn = phys<PHYS>(E0[o - G.w], k - 1, d.nz, S0[ii], B0[ii], d.ri, d.tv);
+                    const double up = phys<PHYS>(E0[o + G.w], k + 1, d.nz, S0[ii], B0[ii], d.ri, d.tv);
+                    s6 = dadd(dadd(s6, dn), up);
+                    out = dadd(dmul(d.c6, c), dmul(d.dv, s6));
+                }
+                urow[ii * d.si + (long long)(k - 1) * d.sk] = out;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[l0 % NS]);
+        }
+        // the segment's last two slabs are no longer needed
+        __syncwarp();
+        if (lane == 0) {
+            mbar_arrive(&empty[L % NS]);
+            mbar_arrive(&empty[(L + 1) % NS]);
+        }
+        L += 2;
+        r += jb - ja + 1;
+    }
+}
+
+} // namespace hftw

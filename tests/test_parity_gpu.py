@@ -1,0 +1,180 @@
+"""GPU parity: the sm_100a path, called through the C ABI, against the oracle.
+
+Bar: BITWISE equality on all four SimState fields (the library uses only
+explicitly rounded IEEE double ops in the reference's association order, so
+the tolerance is exactly 0).  Sources of truth:
+  * tests/golden/*.npz -- outputs of the unmodified reference,
+  * golden FNV-1a-64 hashes at the BASELINE sizes (256x256x64, 1581x1301x58),
+  * the C restatement (oracle/) on fresh seeded random states.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import load_case
+from paper_1802_05839_b200 import weather as W
+
+pytestmark = pytest.mark.gpu
+
+TOL = 0.0  # bitwise
+LAYOUTS = ["ijk", "kij"]
+KERNELS = ["auto", "fused_cell", "split"]
+
+
+def cfg_of(d):
+    return W.GridConfig(**d)
+
+
+def run_device(cfg, steps, layout="ijk", kernel="auto", init_state=None):
+    with W.Context(cfg, layout=layout, kernel=kernel) as ctx:
+        if init_state is None:
+            ctx.init()
+        else:
+            for name, arr in init_state.items():
+                ctx.upload(name, np.ascontiguousarray(arr))
+        ctx.step(steps)
+        return {n: ctx.download(n) for n in ("energy", "energy_u", "energy_surf", "energy_pbl")}
+
+
+def assert_same(got, want, tag):
+    for f in ("energy", "energy_u", "energy_surf", "energy_pbl"):
+        a, b = got[f], want[f]
+        assert a.shape == b.shape, (tag, f)
+        bad = np.flatnonzero(a != b)
+        assert bad.size == 0, f"{tag} {f}: {bad.size} cells differ, first {bad[:5]}, " \
+                              f"max |d| {np.max(np.abs(a - b)):.3e}"
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_golden_cases(golden, layout, kernel):
+    for name, case in golden["full_cases"].items():
+        npz = load_case(name)
+        init = None
+        if case["initial"] != "reference_init":
+            init = {f: npz["in_" + f] for f in ("energy", "energy_u", "energy_surf", "energy_pbl")}
+        got = run_device(cfg_of(case["grid"]), case["steps"], layout, kernel, init)
+        want = {f: npz["out_" + f] for f in ("energy", "energy_u", "energy_surf", "energy_pbl")}
+        assert_same(got, want, f"{name}/{layout}/{kernel}")
+
+
+def test_fused_tma_selected_for_ijk():
+    with W.Context(W.GridConfig(nx=100, ny=40, nz=58)) as ctx:
+        assert ctx.kernel == "fused_tma"
+        assert ctx.launches_per_step == 1
+
+
+@pytest.mark.parametrize("shape", [(100, 37, 58), (130, 5, 3), (64, 64, 2), (2, 2, 2),
+                                   (65, 3, 9), (33, 200, 17), (7, 9, 200), (5, 6, 300),
+                                   (129, 2, 64)])
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_random_states_vs_oracle(coracle, shape, layout):
+    nx, ny, nz = shape
+    rng = np.random.default_rng(nx * 1000 + ny * 10 + nz)
+    cfg = W.GridConfig(nx=nx, ny=ny, nz=nz, diffusion_velocity=float(rng.uniform(0, 1 / 6)),
+                       radiation_intensity=float(rng.uniform(-0.5, 0.5)),
+                       transfer_velocity=float(rng.uniform(0, 0.1)),
+                       surf_energy=float(rng.uniform(250, 350)), pbl_energy=200.0)
+    g = O.grid_from(cfg)
+    n3, n2 = O.shapes(g)
+    s0 = O.State(rng.uniform(150, 350, n3), rng.uniform(150, 350, n3),
+                 rng.uniform(150, 350, n2), rng.uniform(150, 350, n2))
+    want = coracle.steps(g, s0, 3).fields()
+    for kernel in ("auto", "fused_cell", "split"):
+        got = run_device(cfg, 3, layout, kernel, s0.fields())
+        assert_same(got, want, f"{shape}/{layout}/{kernel}")
+
+
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_stencil_config_hash(golden, coracle, layout):
+    h = golden["hashes"]["256x256x64_s10"]
+    got = run_device(cfg_of(h["grid"]), h["steps"], layout)
+    for f, v in h["fnv1a64"].items():
+        assert coracle.fnv(got[f]) == v, f
+
+
+def test_asuca_hash_and_phases(golden, coracle):
+    """BASELINE's full size 1581x1301x58: bitwise via the reference's hashes."""
+    h = golden["hashes"]["1581x1301x58_s2"]
+    cfg = cfg_of(h["grid"])
+    for layout in LAYOUTS:
+        got = run_device(cfg, h["steps"], layout)
+        for f, v in h["fnv1a64"].items():
+            assert coracle.fnv(got[f]) == v, (layout, f)
+    # physics alone (weather.cpp:118-128) from the initial condition, both mappings
+    ph = golden["hashes"]["physics_1581x1301x58_from_init"]["fnv1a64"]["e"]
+    for layout in LAYOUTS:
+        for mode in (0, 1):
+            with W.Context(cfg, layout=layout) as ctx:
+                ctx.init()
+                ctx.physics(mode)
+                assert coracle.fnv(ctx.download("energy")) == ph, (layout, mode)
+
+
+def test_diffusion_only_hash(golden, coracle):
+    d = golden["hashes"]["diffuse_256x256x64_from_s1"]
+    cfg = cfg_of(d["grid"])
+    for layout in LAYOUTS:
+        with W.Context(cfg, layout=layout) as ctx:
+            ctx.init()
+            ctx.step(1)
+            ctx.diffuse()
+            assert coracle.fnv(ctx.download("energy")) == d["fnv1a64"]["u"], layout
+
+
+def test_energy_u_observability(coracle):
+    """energy_u after a step is the post-physics, pre-diffusion field
+    (weather.cpp:118-128 in place, then the swap at :170)."""
+    cfg = W.GridConfig(nx=70, ny=33, nz=12)
+    g = O.grid_from(cfg)
+    with W.Context(cfg) as ctx:
+        ctx.init()
+        assert np.all(ctx.download("energy_u") == 0.0)  # weather.cpp:82
+        ctx.step(2)
+        ref2 = coracle.run_reference(g, 2)
+        assert np.array_equal(ctx.download("energy_u"), ref2.energy_u)
+        # downloading energy_u materialises it; stepping on must be unaffected
+        ctx.step(3)
+        ref5 = coracle.run_reference(g, 5)
+        assert np.array_equal(ctx.download("energy"), ref5.energy)
+        assert np.array_equal(ctx.download("energy_u"), ref5.energy_u)
+        # new boundary fields must not leak into the previous step's energy_u
+        ctx.step(1)
+        ref6 = coracle.run_reference(g, 6)
+        ctx.upload("energy_surf", np.full_like(ref6.energy_surf, 123.0))
+        assert np.array_equal(ctx.download("energy_u"), ref6.energy_u)
+
+
+def test_split_calls_equal_one_call(coracle):
+    cfg = W.GridConfig(nx=90, ny=21, nz=7)
+    with W.Context(cfg) as a, W.Context(cfg) as b:
+        a.init()
+        b.init()
+        a.step(5)
+        for n in (2, 1, 2):
+            b.step(n)
+        for f in ("energy", "energy_u"):
+            assert np.array_equal(a.download(f), b.download(f))
+
+
+def test_reference_api_mirror(coracle):
+    cfg = W.GridConfig(nx=12, ny=9, nz=5)
+    g = O.grid_from(cfg)
+    st = W.run_reference(cfg, 4)
+    ref = coracle.run_reference(g, 4)
+    r = W.compare_fields(st, W.SimState(*(W.ArrayObject(a.bounds, b) for a, b in zip(
+        st.named().values(), ref.fields().values()))))
+    assert r.shape_ok and r.pass_(TOL)
+    s2 = W.SimState.allocate(cfg)
+    W.reference_init(cfg, s2)
+    W.reference_step(cfg, s2)
+    assert np.array_equal(s2.energy.data, coracle.run_reference(g, 1).energy)
+
+
+def test_errors_are_loud():
+    with pytest.raises(W.HftwError):
+        with W.Context(W.GridConfig(nz=300)) as ctx:
+            ctx.set_kernel("fused_tma")  # nz > 256 exceeds the TMA box
+    with W.Context(W.GridConfig()) as ctx:
+        with pytest.raises(W.HftwError):
+            ctx.step(-1)
