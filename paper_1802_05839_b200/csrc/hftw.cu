@@ -28,7 +28,8 @@ namespace {
 thread_local std::string g_err; // errors of calls without a context
 
 constexpr int kFrontPad = 31; // IJK: logical i = 1 lands on a 256-byte boundary
-constexpr int kNCW = 8;       // consumer warps of the TMA kernel
+constexpr int kNCW = 16;      // consumer warps of the TMA kernel
+constexpr int kChunk = 32;    // rows per TMA work unit
 
 } // namespace
 
@@ -64,7 +65,9 @@ struct hftw_ctx {
     int nstrips = 0;
     size_t smem = 0;
     CUtensorMap tm_e[2]{}, tm_sf{}, tm_pb{};
-    int2* d_ranges = nullptr;
+    int* d_sched = nullptr; // work-unit counter + finished-CTA counter
+    int nchunks = 0;
+    int chunk = kChunk;
     long long ghost_cells = 0;
 
     std::string err;
@@ -166,7 +169,7 @@ int setup_tma(hftw_ctx* c) {
     int tx = 0, ns = 0;
     for (int cand : {64, 32}) {
         hftw::SlabGeom G = hftw::slab_geom(cand, nz);
-        int fit = (int)((smem_optin - 1024) / G.stage);
+        int fit = (int)((smem_optin - 1024) / (G.stage + 20));
         if (fit >= 4) {
             tx = cand;
             ns = std::min(fit, 8);
@@ -177,7 +180,7 @@ int setup_tma(hftw_ctx* c) {
     hftw::SlabGeom G = hftw::slab_geom(tx, nz);
     c->tx = tx;
     c->ns = ns;
-    c->smem = (size_t)ns * G.stage + 2 * ns * sizeof(uint64_t);
+    c->smem = (size_t)ns * G.stage + 2 * ns * sizeof(uint64_t) + ns * sizeof(int);
     if (tx == 64) set_tma_attrs<64>(c->smem);
     else set_tma_attrs<32>(c->smem);
 
@@ -195,61 +198,40 @@ int setup_tma(hftw_ctx* c) {
     // tensor maps: e over {Pi, Rows, nz}, sf/pb over {Pi, Rows}
     const cuuint64_t dims3[3] = {(cuuint64_t)c->Pi, (cuuint64_t)c->Rows, (cuuint64_t)nz};
     const cuuint64_t strides3[2] = {(cuuint64_t)c->Pi * 8, (cuuint64_t)(c->Pi * c->Rows) * 8};
-    const cuuint32_t box3[3] = {(cuuint32_t)(tx + 2), 1, (cuuint32_t)nz};
+    const cuuint32_t box3[3] = {(cuuint32_t)G.w, 1, (cuuint32_t)nz};
     const cuuint32_t estr[3] = {1, 1, 1};
     for (int b = 0; b < 2; ++b) {
         CUresult r = enc(&c->tm_e[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->buf[b], dims3,
                          strides3, box3, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
         if (r != CUDA_SUCCESS) return HFTW_OK;
     }
     const cuuint64_t dims2[2] = {(cuuint64_t)c->Pi, (cuuint64_t)c->Rows};
     const cuuint64_t strides2[1] = {(cuuint64_t)c->Pi * 8};
-    const cuuint32_t box2[2] = {(cuuint32_t)(tx + 2), 1};
+    const cuuint32_t box2[2] = {(cuuint32_t)G.w, 1};
     if (enc(&c->tm_sf, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, c->sf, dims2, strides2, box2, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return HFTW_OK;
     if (enc(&c->tm_pb, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, c->pb, dims2, strides2, box2, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return HFTW_OK;
 
-    // Balanced contiguous partition of the (strip, row) sequence: a row of
-    // strip s costs its slab width plus a fixed per-row overhead, and every
-    // strip change costs two extra slabs.  Greedy cut at equal cost.
+    // Dynamic j-major work units (strip x chunk of rows), one persistent CTA
+    // per SM slot; the scheduler counters live in device memory and re-arm
+    // themselves at the end of every launch.
     const long long nx = c->g.nx, ny = c->g.ny;
     const int nstrips = (int)((nx + tx - 1) / tx);
-    const long long rows = (long long)nstrips * ny;
-    int ctas = (int)std::min<long long>((long long)per_sm * c->num_sms, rows);
-    std::vector<double> cost(nstrips);
-    double total = 0;
-    for (int s = 0; s < nstrips; ++s) {
-        long long w = std::min<long long>(tx, nx - (long long)s * tx);
-        cost[s] = (double)(w + 2) * nz + 64.0;
-        total += cost[s] * ny + 2 * cost[s];
+    c->chunk = (int)std::min<long long>(kChunk, ny);
+    c->nchunks = (int)((ny + c->chunk - 1) / c->chunk);
+    const long long units = (long long)nstrips * c->nchunks;
+    int ctas = (int)std::min<long long>((long long)per_sm * c->num_sms, units);
+    if (!c->d_sched) {
+        CUDA_TRY(c, cudaMalloc(&c->d_sched, 2 * sizeof(int)));
+        CUDA_TRY(c, cudaMemset(c->d_sched, 0, 2 * sizeof(int)));
     }
-    std::vector<int2> ranges(ctas);
-    long long r = 0;
-    double acc = 0;
-    for (int b = 0; b < ctas; ++b) {
-        const double target = total * (b + 1) / ctas;
-        const long long begin = r;
-        while (r < rows && (acc < target || r == begin) &&
-               rows - r > (long long)(ctas - b - 1)) {
-            const int s = (int)(r / ny);
-            acc += cost[s] + ((r % ny == 0 || r == begin) ? 2 * cost[s] : 0.0);
-            ++r;
-        }
-        if (b == ctas - 1) r = rows;
-        ranges[b] = make_int2((int)begin, (int)r);
-    }
-    if (c->d_ranges) cudaFree(c->d_ranges);
-    c->d_ranges = nullptr;
-    CUDA_TRY(c, cudaMalloc(&c->d_ranges, sizeof(int2) * ctas));
-    CUDA_TRY(c, cudaMemcpy(c->d_ranges, ranges.data(), sizeof(int2) * ctas,
-                           cudaMemcpyHostToDevice));
     c->ctas = ctas;
     c->nstrips = nstrips;
     c->ghost_cells = (2 * nx + 2 * (ny + 2)) * (long long)nz;
@@ -269,16 +251,17 @@ int launch_fused(hftw_ctx* c, int src, int kernel) {
     Dom d = make_dom(c);
     if (kernel == HFTW_KERNEL_FUSED_TMA) {
         if (!c->tma_ok) return fail(c, HFTW_EUNSUP, "TMA kernel unavailable for this grid/layout");
-        hftw::TmaArgs a{kFrontPad, 1, c->nstrips, c->ns, c->ghost_cells};
+        hftw::TmaArgs a{kFrontPad, 1, c->nstrips, c->nchunks, c->chunk, c->ns, c->ghost_cells,
+                        c->d_sched};
         dim3 block((kNCW + 1) * 32);
         if (c->tx == 64)
             hftw::step_tma_kernel<64, kNCW, PHYS><<<c->ctas, block, c->smem, c->stream>>>(
                 c->tm_e[src], c->tm_sf, c->tm_pb, e3(c, src), e3(c, src ^ 1), sf2(c), pb2(c), d,
-                a, c->d_ranges);
+                a);
         else
             hftw::step_tma_kernel<32, kNCW, PHYS><<<c->ctas, block, c->smem, c->stream>>>(
                 c->tm_e[src], c->tm_sf, c->tm_pb, e3(c, src), e3(c, src ^ 1), sf2(c), pb2(c), d,
-                a, c->d_ranges);
+                a);
     } else {
         const long long n = (c->g.nx + 2) * (c->g.ny + 2) * c->g.nz;
         if (c->layout == HFTW_KIJ)
@@ -448,7 +431,7 @@ void hftw_destroy(hftw_ctx* c) {
     if (c->sf) cudaFree(c->sf);
     if (c->pb) cudaFree(c->pb);
     if (c->staging) cudaFree(c->staging);
-    if (c->d_ranges) cudaFree(c->d_ranges);
+    if (c->d_sched) cudaFree(c->d_sched);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -469,6 +452,7 @@ int hftw_init(hftw_ctx* c) {
             e3(c, c->cur), sf2(c), pb2(c), d, d.nx, d.ny, d.nz, 0, 0, c->g.surf_energy,
             c->g.pbl_energy);
     CUDA_TRY(c, cudaGetLastError());
+    if (c->d_sched) CUDA_TRY(c, cudaMemsetAsync(c->d_sched, 0, 2 * sizeof(int), c->stream));
     c->eu_derived = false; // energy_u is all zeros (weather.cpp:82)
     c->initialized = true;
     return HFTW_OK;

@@ -260,8 +260,8 @@ __global__ void relayout_kernel(const double* __restrict__ src, double* __restri
 // Work decomposition: the interior (i in 1..nx, j in 1..ny) is cut into
 // i-strips of TX cells; a CTA owns a contiguous range of (strip, row) pairs and
 // marches along j.  For every row it streams one SLAB -- the (TX+2) x nz
-// block {i0-1 .. i0+TX} x {j} x {1..nz} -- into shared memory with ONE 3D TMA
-// load (box {TX+2, 1, nz}), plus the matching sf/pb rows.  Row j is computed
+// block {i0-2 .. i0+TX+1} x {j} x {1..nz} -- into shared memory with ONE 3D TMA
+// load (box {TX+4, 1, nz}), plus the matching sf/pb rows.  Row j is computed
 // from slabs j-1, j, j+1 held in an NS-deep mbarrier ring, so each e value
 // crosses HBM once (plus a 2/TX halo share that L2 serves) and u is written
 // once with 256-byte aligned coalesced stores.  The k direction needs no halo
@@ -312,9 +312,14 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         : "memory");
 }
 
-// Shared-memory geometry of one pipeline stage.
+// Shared-memory geometry of one pipeline stage.  A slab row spans logical
+// i0-2 .. i0+TX+1 (TX + 4 doubles): the TMA box must START on a 16-byte
+// boundary (an odd fp64 coordinate faults with an illegal instruction on
+// sm_100a), and the store side keeps i0 on a 256-byte boundary, so the box
+// begins one element before the i0-1 halo.  Column c of a slab row holds
+// logical i = i0 - 2 + c.
 struct SlabGeom {
-    int w;          // TX + 2 doubles per slab row
+    int w;          // TX + 4 doubles per slab row
     int e_bytes;    // slab bytes rounded to 128
     int r_bytes;    // one sf/pb row rounded to 128
     int stage;      // e + sf + pb
@@ -322,7 +327,7 @@ struct SlabGeom {
 };
 __host__ __device__ inline SlabGeom slab_geom(int tx, int nz) {
     SlabGeom g;
-    g.w = tx + 2;
+    g.w = tx + 4;
     g.e_bytes = ((g.w * nz * 8) + 127) / 128 * 128;
     g.r_bytes = ((g.w * 8) + 127) / 128 * 128;
     g.stage = g.e_bytes + 2 * g.r_bytes;
@@ -331,12 +336,21 @@ __host__ __device__ inline SlabGeom slab_geom(int tx, int nz) {
 }
 
 struct TmaArgs {
-    int fp;       // tensor-map i coordinate of logical i = 0
-    int jrow0;    // tensor-map row coordinate of logical j = 0
-    int nstrips;
-    int ns;       // pipeline depth
+    int fp;        // tensor-map i coordinate of logical i = 0
+    int jrow0;     // tensor-map row coordinate of logical j = 0
+    int nstrips;   // i-strips of TX cells over 1..nx
+    int nchunks;   // j-chunks of `chunk` rows over 1..ny
+    int chunk;
+    int ns;        // pipeline depth (stages)
     long long ghost_cells;
+    int* sched;    // [0] next work unit, [1] CTAs finished (self-resetting)
 };
+
+// Post-physics value of a slab element for a cell that is NOT on k = 1 / nz.
+template <bool PHYS>
+__device__ __forceinline__ double pin(double ev, double ri) {
+    return PHYS ? dadd(ev, ri) : ev;
+}
 
 template <int TX, int NCW, bool PHYS>
 __global__ void __launch_bounds__((NCW + 1) * 32, 1)
@@ -344,15 +358,15 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
                     const __grid_constant__ CUtensorMap tm_sf,
                     const __grid_constant__ CUtensorMap tm_pb, const double* __restrict__ e,
                     double* __restrict__ u, const double* __restrict__ sf,
-                    const double* __restrict__ pb, Dom d, TmaArgs a,
-                    const int2* __restrict__ ranges) {
+                    const double* __restrict__ pb, Dom d, TmaArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     const SlabGeom G = slab_geom(TX, d.nz);
     const int NS = a.ns;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NS * G.stage);
     uint64_t* empty = full + NS;
+    int* slot_unit = reinterpret_cast<int*>(empty + NS); // work unit of each staged slab
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int2 rg = ranges[blockIdx.x]; // [begin, end) over linear rows s*ny + (j-1)
+    const int units = a.nstrips * a.nchunks;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < NS; ++s) {
@@ -364,25 +378,45 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     __syncthreads();
 
     if (warp == NCW) {
-        // ---------------- producer warp ----------------
+        // ---------------- producer: work scheduler + TMA issue ----------------
+        // Units are handed out j-major (all strips of chunk 0, then chunk 1, ...)
+        // so the CTAs in flight sweep the grid as one front and the slab
+        // halo columns / chunk-boundary rows another CTA needs are still in L2.
         if (lane == 0) {
             uint32_t L = 0;
-            int r = rg.x;
-            while (r < rg.y) {
-                const int s = r / d.ny, ja = r % d.ny + 1;
-                const int jb = min(d.ny, ja + (rg.y - r) - 1);
-                const int ic = a.fp + 1 + s * TX - 1; // tensor coordinate of i0 - 1
-                for (int jj = ja - 1; jj <= jb + 1; ++jj, ++L) {
+            for (;;) {
+                const int unit = atomicAdd(&a.sched[0], 1);
+                const bool stop = unit >= units;
+                int ja = 0, jb = -1, ic = 0;
+                if (!stop) {
+                    const int ch = unit / a.nstrips, st = unit % a.nstrips;
+                    ja = ch * a.chunk + 1;
+                    jb = min(d.ny, ja + a.chunk - 1);
+                    ic = a.fp + 1 + st * TX - 2; // tensor coordinate of i0 - 2 (even)
+                }
+                for (int jj = ja - 1; stop ? jj == ja - 1 : jj <= jb + 1; ++jj, ++L) {
                     const uint32_t slot = L % NS;
                     if (L >= (uint32_t)NS) mbar_wait(&empty[slot], ((L / NS) - 1) & 1);
-                    unsigned char* st = smem + (size_t)slot * G.stage;
+                    slot_unit[slot] = stop ? -1 : unit;
+                    if (stop) {
+                        mbar_arrive(&full[slot]); // no bytes: tells the consumers to finish
+                        break;
+                    }
+                    unsigned char* stg = smem + (size_t)slot * G.stage;
                     mbar_expect_tx(&full[slot], G.tx_bytes);
-                    tma_load_3d(st, &tm_e, &full[slot], ic, a.jrow0 + jj, 0);
-                    tma_load_2d(st + G.e_bytes, &tm_sf, &full[slot], ic, a.jrow0 + jj);
-                    tma_load_2d(st + G.e_bytes + G.r_bytes, &tm_pb, &full[slot], ic,
+                    tma_load_3d(stg, &tm_e, &full[slot], ic, a.jrow0 + jj, 0);
+                    tma_load_2d(stg + G.e_bytes, &tm_sf, &full[slot], ic, a.jrow0 + jj);
+                    tma_load_2d(stg + G.e_bytes + G.r_bytes, &tm_pb, &full[slot], ic,
                                 a.jrow0 + jj);
                 }
-                r += jb - ja + 1;
+                if (stop) break;
+            }
+            // the last CTA to finish re-arms the scheduler for the next launch
+            __threadfence();
+            if (atomicAdd(&a.sched[1], 1) == (int)gridDim.x - 1) {
+                a.sched[0] = 0;
+                a.sched[1] = 0;
+                __threadfence();
             }
         }
         return;
@@ -414,79 +448,96 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
         }
     }
 
-    constexpr int HALVES = TX / 32;
-    const int items = d.nz * HALVES;
-    uint32_t L = 0; // load index of slab (j - 1) for the current row
-    int r = rg.x;
-    while (r < rg.y) {
-        const int s = r / d.ny, ja = r % d.ny + 1;
-        const int jb = min(d.ny, ja + (rg.y - r) - 1);
-        const int i0 = 1 + s * TX;
-        const int width = min(TX, d.nx - i0 + 1);
-        for (int j = ja; j <= jb; ++j, ++L) {
-            const uint32_t l0 = L, l1 = L + 1, l2 = L + 2;
-            if (j == ja) {
-                mbar_wait(&full[l0 % NS], (l0 / NS) & 1);
-                mbar_wait(&full[l1 % NS], (l1 / NS) & 1);
-            }
+    // Thread -> (column c of the strip, k-group g).  A warp is 32 consecutive
+    // columns at one k, so every smem access and every u store is a
+    // contiguous 256-byte run; each thread walks its k-range with a
+    // three-value register window (P(k-1), P(k), P(k+1)).
+    constexpr int NKG = NCW * 32 / TX;
+    const int c = threadIdx.x % TX, g = threadIdx.x / TX;
+    const int nz = d.nz;
+    const int kl = 1 + (g * nz) / NKG, kh = ((g + 1) * nz) / NKG;
+    const int w = G.w, cc = c + 2; // slab column of cell i0 + c
+    const double ri = d.ri, tv = d.tv, dv = d.dv, c5 = d.c5, c6 = d.c6;
+
+    uint32_t L = 0; // load index of the first slab of the current unit
+    for (;;) {
+        {
+            const uint32_t slot = L % NS;
+            mbar_wait(&full[slot], (L / NS) & 1);
+        }
+        const int unit = slot_unit[L % NS];
+        if (unit < 0) break;
+        const int ch = unit / a.nstrips, st = unit % a.nstrips;
+        const int ja = ch * a.chunk + 1, jb = min(d.ny, ja + a.chunk - 1);
+        const int i0 = 1 + st * TX;
+        const bool active = c < min(TX, d.nx - i0 + 1) && kl <= kh;
+        for (int j = ja; j <= jb; ++j) {
+            const uint32_t l0 = L + (j - ja), l1 = l0 + 1, l2 = l0 + 2;
+            if (j == ja) mbar_wait(&full[l1 % NS], (l1 / NS) & 1);
             mbar_wait(&full[l2 % NS], (l2 / NS) & 1);
-            const unsigned char* stm = smem + (size_t)(l0 % NS) * G.stage;
-            const unsigned char* st0 = smem + (size_t)(l1 % NS) * G.stage;
-            const unsigned char* stp = smem + (size_t)(l2 % NS) * G.stage;
-            const double* Em = reinterpret_cast<const double*>(stm);
-            const double* E0 = reinterpret_cast<const double*>(st0);
-            const double* Ep = reinterpret_cast<const double*>(stp);
-            const double* Sm = reinterpret_cast<const double*>(stm + G.e_bytes);
-            const double* S0 = reinterpret_cast<const double*>(st0 + G.e_bytes);
-            const double* Sp = reinterpret_cast<const double*>(stp + G.e_bytes);
-            const double* Bm = reinterpret_cast<const double*>(stm + G.e_bytes + G.r_bytes);
-            const double* B0 = reinterpret_cast<const double*>(st0 + G.e_bytes + G.r_bytes);
-            const double* Bp = reinterpret_cast<const double*>(stp + G.e_bytes + G.r_bytes);
-            double* urow = u + (long long)(i0 - 1) * d.si + (long long)j * d.sj;
-            for (int it = warp; it < items; it += NCW) {
-                const int k = it / HALVES + 1;
-                const int ii = 1 + (it % HALVES) * 32 + lane; // slab column; 0 is i0-1
-                if (ii > width) continue;
-                const int o = (k - 1) * G.w + ii;
-                double c, s6;
-                if (!PHYS || (k != 1 && k != d.nz)) {
-                    c = phys<PHYS>(E0[o], k, d.nz, 0.0, 0.0, d.ri, d.tv);
-                    s6 = dadd(phys<PHYS>(E0[o - 1], k, d.nz, 0.0, 0.0, d.ri, d.tv),
-                              phys<PHYS>(E0[o + 1], k, d.nz, 0.0, 0.0, d.ri, d.tv));
-                    s6 = dadd(s6, phys<PHYS>(Em[o], k, d.nz, 0.0, 0.0, d.ri, d.tv));
-                    s6 = dadd(s6, phys<PHYS>(Ep[o], k, d.nz, 0.0, 0.0, d.ri, d.tv));
-                } else {
-                    c = phys<PHYS>(E0[o], k, d.nz, S0[ii], B0[ii], d.ri, d.tv);
-                    s6 = dadd(phys<PHYS>(E0[o - 1], k, d.nz, S0[ii - 1], B0[ii - 1], d.ri, d.tv),
-                              phys<PHYS>(E0[o + 1], k, d.nz, S0[ii + 1], B0[ii + 1], d.ri, d.tv));
-                    s6 = dadd(s6, phys<PHYS>(Em[o], k, d.nz, Sm[ii], Bm[ii], d.ri, d.tv));
-                    s6 = dadd(s6, phys<PHYS>(Ep[o], k, d.nz, Sp[ii], Bp[ii], d.ri, d.tv));
+            if (active) {
+                const unsigned char* stm = smem + (size_t)(l0 % NS) * G.stage;
+                const unsigned char* st0 = smem + (size_t)(l1 % NS) * G.stage;
+                const unsigned char* stp = smem + (size_t)(l2 % NS) * G.stage;
+                const double* em = reinterpret_cast<const double*>(stm) + cc;
+                const double* e0 = reinterpret_cast<const double*>(st0) + cc;
+                const double* ep = reinterpret_cast<const double*>(stp) + cc;
+                const double* Sm = reinterpret_cast<const double*>(stm + G.e_bytes) + cc;
+                const double* S0 = reinterpret_cast<const double*>(st0 + G.e_bytes) + cc;
+                const double* Sp = reinterpret_cast<const double*>(stp + G.e_bytes) + cc;
+                const double* Bm = reinterpret_cast<const double*>(stm + G.e_bytes + G.r_bytes) + cc;
+                const double* B0 = reinterpret_cast<const double*>(st0 + G.e_bytes + G.r_bytes) + cc;
+                const double* Bp = reinterpret_cast<const double*>(stp + G.e_bytes + G.r_bytes) + cc;
+                // centre-column post-physics value at any k (boundary-aware)
+                auto Pc = [&](int kk) {
+                    return phys<PHYS>(e0[(kk - 1) * w], kk, nz, S0[0], B0[0], ri, tv);
+                };
+                double* up = u + (long long)(i0 + c) * d.si + (long long)j * d.sj +
+                             (long long)(kl - 1) * d.sk;
+                double pd = kl > 1 ? Pc(kl - 1) : 0.0;
+                double pc = Pc(kl);
+                for (int k = kl; k <= kh; ++k) {
+                    const int o = (k - 1) * w;
+                    double out, pn;
+                    if (k >= 2 && k <= nz - 2) {
+                        // fast path: no boundary physics involved
+                        pn = pin<PHYS>(e0[o + w], ri);
+                        double s6 = dadd(pin<PHYS>(e0[o - 1], ri), pin<PHYS>(e0[o + 1], ri));
+                        s6 = dadd(s6, pin<PHYS>(em[o], ri));
+                        s6 = dadd(s6, pin<PHYS>(ep[o], ri));
+                        s6 = dadd(dadd(s6, pd), pn);
+                        out = dadd(dmul(c6, pc), dmul(dv, s6));
+                    } else {
+                        pn = k < nz ? Pc(k + 1) : 0.0;
+                        double s6 = dadd(phys<PHYS>(e0[o - 1], k, nz, S0[-1], B0[-1], ri, tv),
+                                         phys<PHYS>(e0[o + 1], k, nz, S0[1], B0[1], ri, tv));
+                        s6 = dadd(s6, phys<PHYS>(em[o], k, nz, Sm[0], Bm[0], ri, tv));
+                        s6 = dadd(s6, phys<PHYS>(ep[o], k, nz, Sp[0], Bp[0], ri, tv));
+                        if (k == 1) { // weather.cpp:142-145
+                            out = dadd(dmul(c5, pc), dmul(dv, dadd(s6, pn)));
+                        } else if (k == nz) { // weather.cpp:146-149
+                            out = dadd(dmul(c5, pc), dmul(dv, dadd(s6, pd)));
+                        } else { // weather.cpp:134-137
+                            out = dadd(dmul(c6, pc), dmul(dv, dadd(dadd(s6, pd), pn)));
+                        }
+                    }
+                    *up = out;
+                    up += d.sk;
+                    pd = pc;
+                    pc = pn;
                 }
-                double out;
-                if (k == 1 || k == d.nz) {
-                    const int kk = k == 1 ? 2 : d.nz - 1;
-                    const int ok = (kk - 1) * G.w + ii;
-                    s6 = dadd(s6, phys<PHYS>(E0[ok], kk, d.nz, S0[ii], B0[ii], d.ri, d.tv));
-                    out = dadd(dmul(d.c5, c), dmul(d.dv, s6));
-                } else {
-                    const double dn = phys<PHYS>(E0[o - G.w], k - 1, d.nz, S0[ii], B0[ii], d.ri, d.tv);
-                    const double up = phys<PHYS>(E0[o + G.w], k + 1, d.nz, S0[ii], B0[ii], d.ri, d.tv);
-                    s6 = dadd(dadd(s6, dn), up);
-                    out = dadd(dmul(d.c6, c), dmul(d.dv, s6));
-                }
-                urow[ii * d.si + (long long)(k - 1) * d.sk] = out;
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[l0 % NS]);
         }
-        // the segment's last two slabs are no longer needed
+        // the unit's last two slabs are no longer needed
+        const uint32_t lend = L + (jb - ja + 1);
         __syncwarp();
         if (lane == 0) {
-            mbar_arrive(&empty[L % NS]);
-            mbar_arrive(&empty[(L + 1) % NS]);
+            mbar_arrive(&empty[lend % NS]);
+            mbar_arrive(&empty[(lend + 1) % NS]);
         }
-        L += 2;
-        r += jb - ja + 1;
+        L = lend + 2;
     }
 }
 
