@@ -1,0 +1,189 @@
+//------------------------------------------------------------------------------
+// hft_b200/weather.hpp -- header-only C++ adapter over the C ABI (hftw.h).
+//
+// Drop-in for the reference's native simulator API
+// (/root/reference/proj/include/hft/weather.hpp, namespace hft):
+//
+//   hft::validate(cfg, diags)          (weather.hpp:37)  -> hft::b200::validate
+//   hft::reference_init(cfg, st)       (weather.hpp:51)  -> hft::b200::reference_init
+//   hft::reference_step(cfg, st)       (weather.hpp:55)  -> hft::b200::reference_step
+//   hft::run_reference(cfg, steps)     (weather.hpp:59)  -> hft::b200::run_reference
+//
+// The functions are templates over the caller's types, so they accept the
+// reference's own hft::GridConfig / hft::SimState / hft::Diagnostics
+// unchanged (anything with the same member names works: GridConfig's ten
+// fields, SimState's four ArrayObject members with `bounds` and `data`,
+// a Diagnostics with error(SourceRef, std::string)).  For code that does not
+// link the reference, hft::b200 also defines minimal look-alike types.
+//
+// Results are bitwise identical to the reference (see include/hftw.h).
+// Unlike the reference, device work can fail (no GPU, out of memory): the
+// adapter throws hft::b200::Error -- there is no CPU fallback.
+//------------------------------------------------------------------------------
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../hftw.h"
+
+namespace hft::b200 {
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+inline void check(int rc, const hftw_ctx* ctx = nullptr) {
+    if (rc != HFTW_OK) throw Error(rc, hftw_last_error(ctx));
+}
+
+// ---- minimal look-alike types (same member names as the reference) --------
+struct GridConfig {
+    long long nx = 16, ny = 16, nz = 8;
+    double timestep = 0.1;
+    double output_timestep = 1.0;
+    double diffusion_velocity = 0.1;
+    double radiation_intensity = 0.1;
+    double transfer_velocity = 0.01;
+    double surf_energy = 330.0;
+    double pbl_energy = 200.0;
+};
+struct ArrayObject {
+    std::vector<std::pair<long long, long long>> bounds;
+    std::vector<double> data;
+};
+struct SimState {
+    ArrayObject energy, energy_u, energy_surf, energy_pbl;
+};
+
+// ---- conversions -----------------------------------------------------------
+template <class Cfg>
+hftw_grid to_grid(const Cfg& c) {
+    hftw_grid g;
+    g.nx = c.nx;
+    g.ny = c.ny;
+    g.nz = c.nz;
+    g.timestep = c.timestep;
+    g.output_timestep = c.output_timestep;
+    g.diffusion_velocity = c.diffusion_velocity;
+    g.radiation_intensity = c.radiation_intensity;
+    g.transfer_velocity = c.transfer_velocity;
+    g.surf_energy = c.surf_energy;
+    g.pbl_energy = c.pbl_energy;
+    return g;
+}
+
+// Shapes of weather.cpp:71 (3D) and :77 (2D).
+template <class Cfg, class Array>
+void shape3(const Cfg& c, Array& a) {
+    a.bounds = {{0, c.nx + 1}, {0, c.ny + 1}, {1, c.nz}};
+    a.data.assign(static_cast<std::size_t>((c.nx + 2) * (c.ny + 2) * c.nz), 0.0);
+}
+template <class Cfg, class Array>
+void shape2(const Cfg& c, Array& a) {
+    a.bounds = {{0, c.nx + 1}, {0, c.ny + 1}};
+    a.data.assign(static_cast<std::size_t>((c.nx + 2) * (c.ny + 2)), 0.0);
+}
+
+/// hft::validate (weather.cpp:24-41): same rules and messages, reported as
+/// diags.error({"<config>", 0}, message).
+template <class Cfg, class Diags>
+bool validate(const Cfg& cfg, Diags& diags) {
+    hftw_grid g = to_grid(cfg);
+    char msg[2048];
+    int rc = hftw_validate(&g, msg, sizeof msg);
+    std::string all(msg), prefix("<config>: error: ");
+    std::size_t pos = 0;
+    while (pos < all.size()) {
+        std::size_t nl = all.find('\n', pos);
+        std::string line = all.substr(pos, nl == std::string::npos ? std::string::npos : nl - pos);
+        if (line.rfind(prefix, 0) == 0) line = line.substr(prefix.size());
+        if (!line.empty()) diags.error({"<config>", 0}, line);
+        if (nl == std::string::npos) break;
+        pos = nl + 1;
+    }
+    return rc == HFTW_OK;
+}
+
+/// Device-resident simulation (new API): state lives in HBM between steps.
+class Simulation {
+public:
+    template <class Cfg>
+    explicit Simulation(const Cfg& cfg, int layout = HFTW_IJK, int device = 0)
+        : grid_(to_grid(cfg)) {
+        check(hftw_create(&grid_, layout, device, &ctx_));
+    }
+    Simulation(const Simulation&) = delete;
+    Simulation& operator=(const Simulation&) = delete;
+    ~Simulation() { hftw_destroy(ctx_); }
+
+    void init() { check(hftw_init(ctx_), ctx_); }
+    void step(long long n = 1) { check(hftw_step(ctx_, n), ctx_); }
+    void sync() { check(hftw_sync(ctx_), ctx_); }
+    void set_kernel(int k) { check(hftw_set_kernel(ctx_, k), ctx_); }
+
+    template <class State>
+    void upload(const State& st) {
+        check(hftw_upload(ctx_, HFTW_ENERGY, st.energy.data.data()), ctx_);
+        check(hftw_upload(ctx_, HFTW_ENERGY_U, st.energy_u.data.data()), ctx_);
+        check(hftw_upload(ctx_, HFTW_ENERGY_SURF, st.energy_surf.data.data()), ctx_);
+        check(hftw_upload(ctx_, HFTW_ENERGY_PBL, st.energy_pbl.data.data()), ctx_);
+    }
+    /// Fill a SimState (shapes set as reference_init would).
+    template <class State>
+    void download(State& st) {
+        GridConfig c;
+        c.nx = grid_.nx;
+        c.ny = grid_.ny;
+        c.nz = grid_.nz;
+        shape3(c, st.energy);
+        shape3(c, st.energy_u);
+        shape2(c, st.energy_surf);
+        shape2(c, st.energy_pbl);
+        check(hftw_download(ctx_, HFTW_ENERGY, st.energy.data.data()), ctx_);
+        check(hftw_download(ctx_, HFTW_ENERGY_U, st.energy_u.data.data()), ctx_);
+        check(hftw_download(ctx_, HFTW_ENERGY_SURF, st.energy_surf.data.data()), ctx_);
+        check(hftw_download(ctx_, HFTW_ENERGY_PBL, st.energy_pbl.data.data()), ctx_);
+    }
+    hftw_ctx* handle() { return ctx_; }
+
+private:
+    hftw_grid grid_;
+    hftw_ctx* ctx_ = nullptr;
+};
+
+/// hft::reference_init (weather.cpp:67-99), computed on the device.
+template <class Cfg, class State>
+void reference_init(const Cfg& cfg, State& st, int device = 0) {
+    Simulation s(cfg, HFTW_IJK, device);
+    s.init();
+    s.download(st);
+}
+
+/// hft::reference_step (weather.cpp:101-171) on a host SimState, in place.
+/// Transfer-bound by construction; keep state on the device (Simulation) for
+/// runs of more than one step.
+template <class Cfg, class State>
+void reference_step(const Cfg& cfg, State& st, int device = 0) {
+    Simulation s(cfg, HFTW_IJK, device);
+    s.upload(st);
+    s.step(1);
+    s.download(st);
+}
+
+/// hft::run_reference (weather.cpp:173-178).
+template <class State = SimState, class Cfg>
+State run_reference(const Cfg& cfg, long long steps, int device = 0) {
+    Simulation s(cfg, HFTW_IJK, device);
+    s.init();
+    s.step(steps);
+    State st;
+    s.download(st);
+    return st;
+}
+
+} // namespace hft::b200
