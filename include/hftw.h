@@ -150,6 +150,51 @@ int hftw_launches_per_step(const hftw_ctx* ctx);
  * (i=0, j=0, k=1) and element strides (si, sj, sk); sk = 0 for 2D fields. */
 int hftw_field_view(hftw_ctx* ctx, int field, void** dptr, int64_t strides[3]);
 
+/* ---- multi-GPU: 2D horizontal (I x J) decomposition, one process per GPU ----
+ *
+ * The paper's ASUCA decomposition, not implemented by the
+ * reference: full k columns per rank, px x py ranks, rank =
+ * ry * px + rx.  Rank r of p owns inner indices 1 + floor(r*n/p) ..
+ * floor((r+1)*n/p); rank 0 also owns ghost 0 and rank p-1 ghost n+1.  The
+ * cyclic ghost rules (weather.cpp:152-168) become a torus: each rank pushes its
+ * first/last inner column and row of every new field into the neighbours'
+ * halo slots (pre-physics values; physics of halo cells is recomputed from
+ * static sf/pb halos), and a per-direction step flag orders the pushes.  The
+ * result is bitwise identical to the single-domain run. */
+enum hftw_dir { HFTW_W = 0, HFTW_E = 1, HFTW_S = 2, HFTW_N = 3 };
+
+typedef struct hftw_plan {
+    int32_t px, py, rx, ry, rank;
+    int64_t gi0, gj0;            /* global index of local i = 0 / j = 0 */
+    int64_t lnx, lny;            /* owned inner extents */
+    int32_t own_w, own_e, own_s, own_n; /* owns the global ghost column / row */
+    int32_t wfar, efar, sfar, nfar;     /* local index of a ghost cell's cyclic partner */
+    int32_t nbr[4];              /* neighbour rank per hftw_dir, -1 = cyclic partner is local */
+    int32_t send_slot[4];        /* my face lands in the neighbour at this local column (W/E) or row (S/N) */
+    int64_t face_lo[4], face_hi[4]; /* local range along each face (j for W/E, i for S/N) */
+} hftw_plan;
+
+/* Host-only (no GPU needed): the plan of `rank` in a px x py decomposition. */
+int hftw_plan_rank(const hftw_grid* grid, int px, int py, int rank, hftw_plan* out);
+
+/* Create the context of one rank's subdomain on `device`.  Host buffers of
+ * upload/download stay GLOBAL logical arrays; a rank reads/writes only the
+ * cells it owns.  Peers must be connected before init/upload/step. */
+int hftw_create_dist(const hftw_grid* grid, int layout, int device, int px, int py, int rank,
+                     hftw_ctx** out);
+/* Bytes of this rank's exported peer descriptor (CUDA IPC handles + geometry). */
+size_t hftw_peer_desc_size(void);
+/* Export this rank's descriptor into `desc` (hftw_peer_desc_size() bytes). */
+int hftw_peer_export(hftw_ctx* ctx, void* desc);
+/* Map the neighbours: `all` holds every rank's descriptor back to back in rank order. */
+int hftw_peer_connect(hftw_ctx* ctx, const void* all, int world);
+/* Push the current energy and the static sf/pb faces to the neighbours'
+ * halo slots and wait for completion.  The caller brackets it with a
+ * process barrier (after every rank's upload/init, before the next step). */
+int hftw_exchange(hftw_ctx* ctx);
+/* This rank's plan. */
+int hftw_get_plan(const hftw_ctx* ctx, hftw_plan* out);
+
 #ifdef __cplusplus
 }
 #endif

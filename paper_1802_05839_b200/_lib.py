@@ -31,6 +31,30 @@ class hftw_grid(C.Structure):
                 ("pbl_energy", C.c_double)]
 
 
+class hftw_plan(C.Structure):
+    """hftw_plan (include/hftw.h): one rank's subdomain of a px x py decomposition."""
+
+    _fields_ = [("px", C.c_int32), ("py", C.c_int32), ("rx", C.c_int32), ("ry", C.c_int32),
+                ("rank", C.c_int32), ("gi0", C.c_int64), ("gj0", C.c_int64),
+                ("lnx", C.c_int64), ("lny", C.c_int64),
+                ("own_w", C.c_int32), ("own_e", C.c_int32), ("own_s", C.c_int32),
+                ("own_n", C.c_int32), ("wfar", C.c_int32), ("efar", C.c_int32),
+                ("sfar", C.c_int32), ("nfar", C.c_int32), ("nbr", C.c_int32 * 4),
+                ("send_slot", C.c_int32 * 4), ("face_lo", C.c_int64 * 4),
+                ("face_hi", C.c_int64 * 4)]
+
+    def to_dict(self):
+        d = {}
+        for f, _ in self._fields_:
+            v = getattr(self, f)
+            d[f] = list(v) if isinstance(v, C.Array) else v
+        return d
+
+
+W, E, S, N = range(4)
+DIRS = {"w": W, "e": E, "s": S, "n": N}
+
+
 class HftwError(RuntimeError):
     def __init__(self, code: int, msg: str):
         super().__init__(f"hftw error {ERRORS.get(code, code)}: {msg}")
@@ -61,6 +85,15 @@ SIGNATURES = [
     ("hftw_algorithmic_bytes", C.c_double, [_P, C.c_int]),
     ("hftw_launches_per_step", C.c_int, [_P]),
     ("hftw_field_view", C.c_int, [_P, C.c_int, C.POINTER(_P), C.POINTER(C.c_int64)]),
+    ("hftw_plan_rank", C.c_int, [C.POINTER(hftw_grid), C.c_int, C.c_int, C.c_int,
+                                 C.POINTER(hftw_plan)]),
+    ("hftw_create_dist", C.c_int, [C.POINTER(hftw_grid), C.c_int, C.c_int, C.c_int, C.c_int,
+                                   C.c_int, C.POINTER(_P)]),
+    ("hftw_peer_desc_size", C.c_size_t, []),
+    ("hftw_peer_export", C.c_int, [_P, _P]),
+    ("hftw_peer_connect", C.c_int, [_P, _P, C.c_int]),
+    ("hftw_exchange", C.c_int, [_P]),
+    ("hftw_get_plan", C.c_int, [_P, C.POINTER(hftw_plan)]),
 ]
 
 _lib = None

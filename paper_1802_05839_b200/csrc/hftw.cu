@@ -7,6 +7,9 @@
 // The reference's SimState owns host std::vectors and swaps them each step
 // (weather.cpp:170); here the context owns device-resident, padded fields in
 // a ping-pong pair and the caller moves data in/out with upload/download.
+// A context covers either the whole grid or one rank's subdomain of a
+// px x py decomposition (hftw_create_dist); the single-GPU case is the 1 x 1
+// plan, so both share every code path.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -15,6 +18,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -22,6 +26,7 @@
 #include "weather_kernels.cuh"
 
 using hftw::Dom;
+using hftw::Halo;
 
 namespace {
 
@@ -31,19 +36,42 @@ constexpr int kFrontPad = 31; // IJK: logical i = 1 lands on a 256-byte boundary
 constexpr int kNCW = 16;      // consumer warps of the TMA kernel
 constexpr int kChunk = 32;    // rows per TMA work unit
 
+// What a rank publishes to its neighbours (raw bytes through the caller's
+// allgather): IPC handles of the two energy buffers, sf, pb and the flags,
+// plus the geometry needed to address their halo slots.
+struct PeerDesc {
+    cudaIpcMemHandle_t buf[2], sf, pb, flags;
+    long long off3, off2, si, sj, sk, s2j;
+    hftw_plan plan;
+    int magic;
+};
+constexpr int kPeerMagic = 0x48465457; // "HFTW"
+
+struct PeerMap {
+    int rank = -1;
+    double* buf[2] = {nullptr, nullptr}; // at the neighbour's logical (0,0,1)
+    double* sf = nullptr;                // at its logical (0,0)
+    double* pb = nullptr;
+    unsigned long long* flags = nullptr;
+    long long si = 0, sj = 0, sk = 0, s2j = 0;
+};
+
 } // namespace
 
 struct hftw_ctx {
-    hftw_grid g{};
+    hftw_grid g{};       // GLOBAL grid configuration
+    hftw_plan plan{};    // this context's subdomain (1 x 1 plan on one GPU)
+    bool dist = false;
     int layout = HFTW_IJK;
     int device = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     int kernel_req = HFTW_KERNEL_AUTO;
     int num_sms = 148;
+    long long lnx = 0, lny = 0, nz = 0; // local extents
 
     // geometry (elements)
-    long long Pi = 0, Rows = 0;  // IJK row pitch, rows per plane (ny + 4)
+    long long Pi = 0, Rows = 0;  // IJK row pitch, rows per plane (lny + 4)
     long long Pk = 0;            // KIJ column pitch
     long long si = 0, sj = 0, sk = 0, s2j = 0;
     long long off3 = 0, off2 = 0; // offset of logical (0,0,1) / (0,0) from allocation start
@@ -52,10 +80,10 @@ struct hftw_ctx {
     double* buf[2] = {nullptr, nullptr};
     double* sf = nullptr;
     double* pb = nullptr;
-    double* staging = nullptr; // dense logical staging for the KIJ relayout
+    double* staging = nullptr; // dense staging for the KIJ relayout
+    size_t staging_n = 0;
     int cur = 0;               // buf[cur] holds SimState::energy
     bool eu_derived = false;   // energy_u == physics(buf[cur ^ 1]), not yet materialised
-    bool initialized = false;
 
     // TMA kernel state
     bool tma_ok = false;
@@ -69,6 +97,15 @@ struct hftw_ctx {
     int nchunks = 0;
     int chunk = kChunk;
     long long ghost_cells = 0;
+
+    // decomposed run
+    unsigned long long* flags = nullptr; // [4] step flags written by the neighbours
+    int* done = nullptr;                 // CTAs finished in the current launch
+    PeerMap peer[4];
+    std::vector<void*> ipc_opened;
+    bool connected = false;
+    bool halo_dirty = false;             // fields changed since the last exchange
+    long long step_count = 0;            // steps since the last exchange
 
     std::string err;
 };
@@ -97,20 +134,23 @@ int fail(hftw_ctx* c, int code, const char* fmt, ...) {
 bool valid_field(int f) { return f >= HFTW_ENERGY && f <= HFTW_ENERGY_PBL; }
 
 Dom make_dom(const hftw_ctx* c) {
+    const hftw_plan& p = c->plan;
     Dom d{};
-    d.nx = (int)c->g.nx;
-    d.ny = (int)c->g.ny;
-    d.nz = (int)c->g.nz;
+    d.nx = (int)c->lnx;
+    d.ny = (int)c->lny;
+    d.nz = (int)c->nz;
     d.si = c->si;
     d.sj = c->sj;
     d.sk = c->sk;
     d.s2j = c->s2j;
-    d.own_w = d.own_e = d.own_s = d.own_n = 1;
-    // one domain: the cyclic partners are local (weather.cpp:155-167)
-    d.wfar = d.nx;
-    d.efar = 1;
-    d.sfar = d.ny;
-    d.nfar = 1;
+    d.own_w = p.own_w;
+    d.own_e = p.own_e;
+    d.own_s = p.own_s;
+    d.own_n = p.own_n;
+    d.wfar = p.wfar;
+    d.efar = p.efar;
+    d.sfar = p.sfar;
+    d.nfar = p.nfar;
     const double dv = c->g.diffusion_velocity;
     d.ri = c->g.radiation_intensity;
     d.tv = c->g.transfer_velocity;
@@ -123,6 +163,27 @@ Dom make_dom(const hftw_ctx* c) {
     return d;
 }
 
+// Halo parameters of a launch that writes buffer `dst`.
+Halo make_halo(const hftw_ctx* c, int dst) {
+    Halo h{};
+    h.active = c->dist ? 1 : 0;
+    if (!c->dist) return h;
+    for (int d = 0; d < 4; ++d) {
+        const PeerMap& m = c->peer[d];
+        if (m.rank < 0) continue;
+        h.nb[d] = m.buf[dst];
+        h.nsi[d] = m.si;
+        h.nsj[d] = m.sj;
+        h.nsk[d] = m.sk;
+        h.slot[d] = c->plan.send_slot[d];
+        h.nb_flags[d] = m.flags;
+    }
+    h.my_flags = c->flags;
+    h.done = c->done;
+    h.step = c->step_count;
+    return h;
+}
+
 double* e3(const hftw_ctx* c, int b) { return c->buf[b] + c->off3; }
 double* sf2(const hftw_ctx* c) { return c->sf + c->off2; }
 double* pb2(const hftw_ctx* c) { return c->pb + c->off2; }
@@ -131,6 +192,16 @@ int grid_for(const hftw_ctx* c, long long n) {
     long long blocks = (n + 255) / 256;
     long long cap = (long long)c->num_sms * 16;
     return (int)std::max<long long>(1, std::min(blocks, cap));
+}
+
+// owned index ranges of the local domain
+struct Box {
+    long long i0, i1, j0, j1;
+};
+Box owned_box(const hftw_ctx* c) {
+    const hftw_plan& p = c->plan;
+    return {p.own_w ? 0 : 1, p.own_e ? c->lnx + 1 : c->lnx, p.own_s ? 0 : 1,
+            p.own_n ? c->lny + 1 : c->lny};
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -154,18 +225,18 @@ void set_tma_attrs(size_t smem) {
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
-// Choose the TMA kernel geometry and build tensor maps + the per-CTA row
-// ranges.  Leaves tma_ok = false (the cell kernel is used) when the grid does
-// not fit: nz > 256 (TMA box limit) or a 4-stage ring would not fit smem.
+// Choose the TMA kernel geometry and build the tensor maps.  Leaves
+// tma_ok = false (the cell kernel is used) when the grid does not fit: nz >
+// 256 (TMA box limit) or a 4-stage ring would not fit shared memory.
 int setup_tma(hftw_ctx* c) {
     c->tma_ok = false;
-    if (c->layout != HFTW_IJK || c->g.nz > 256) return HFTW_OK;
+    if (c->layout != HFTW_IJK || c->nz > 256) return HFTW_OK;
     auto enc = encode_fn();
     if (!enc) return HFTW_OK;
     int smem_optin = 0;
     CUDA_TRY(c, cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin,
                                        c->device));
-    const int nz = (int)c->g.nz;
+    const int nz = (int)c->nz;
     int tx = 0, ns = 0;
     for (int cand : {64, 32}) {
         hftw::SlabGeom G = hftw::slab_geom(cand, nz);
@@ -195,7 +266,9 @@ int setup_tma(hftw_ctx* c) {
         return HFTW_OK;
     }
 
-    // tensor maps: e over {Pi, Rows, nz}, sf/pb over {Pi, Rows}
+    // tensor maps: e over {Pi, Rows, nz}, sf/pb over {Pi, Rows}; no L2
+    // promotion (a slab row is 68 doubles; 256-byte promotion would read
+    // whole neighbouring granules and inflate HBM traffic)
     const cuuint64_t dims3[3] = {(cuuint64_t)c->Pi, (cuuint64_t)c->Rows, (cuuint64_t)nz};
     const cuuint64_t strides3[2] = {(cuuint64_t)c->Pi * 8, (cuuint64_t)(c->Pi * c->Rows) * 8};
     const cuuint32_t box3[3] = {(cuuint32_t)G.w, 1, (cuuint32_t)nz};
@@ -222,7 +295,7 @@ int setup_tma(hftw_ctx* c) {
     // Dynamic j-major work units (strip x chunk of rows), one persistent CTA
     // per SM slot; the scheduler counters live in device memory and re-arm
     // themselves at the end of every launch.
-    const long long nx = c->g.nx, ny = c->g.ny;
+    const long long nx = c->lnx, ny = c->lny;
     const int nstrips = (int)((nx + tx - 1) / tx);
     c->chunk = (int)std::min<long long>(kChunk, ny);
     c->nchunks = (int)((ny + c->chunk - 1) / c->chunk);
@@ -232,15 +305,19 @@ int setup_tma(hftw_ctx* c) {
         CUDA_TRY(c, cudaMalloc(&c->d_sched, 2 * sizeof(int)));
         CUDA_TRY(c, cudaMemset(c->d_sched, 0, 2 * sizeof(int)));
     }
+    Box o = owned_box(c);
     c->ctas = ctas;
     c->nstrips = nstrips;
-    c->ghost_cells = (2 * nx + 2 * (ny + 2)) * (long long)nz;
+    c->ghost_cells = ((long long)(c->plan.own_s + c->plan.own_n) * nx +
+                      (long long)(c->plan.own_w + c->plan.own_e) * (o.j1 - o.j0 + 1)) *
+                     c->nz;
     c->tma_ok = true;
     return HFTW_OK;
 }
 
 int resolved_kernel(const hftw_ctx* c) {
-    if (c->kernel_req == HFTW_KERNEL_AUTO) return c->tma_ok ? HFTW_KERNEL_FUSED_TMA : HFTW_KERNEL_FUSED_CELL;
+    if (c->kernel_req == HFTW_KERNEL_AUTO)
+        return c->tma_ok ? HFTW_KERNEL_FUSED_TMA : HFTW_KERNEL_FUSED_CELL;
     return c->kernel_req;
 }
 
@@ -249,6 +326,7 @@ int resolved_kernel(const hftw_ctx* c) {
 template <bool PHYS>
 int launch_fused(hftw_ctx* c, int src, int kernel) {
     Dom d = make_dom(c);
+    Halo h = make_halo(c, src ^ 1);
     if (kernel == HFTW_KERNEL_FUSED_TMA) {
         if (!c->tma_ok) return fail(c, HFTW_EUNSUP, "TMA kernel unavailable for this grid/layout");
         hftw::TmaArgs a{kFrontPad, 1, c->nstrips, c->nchunks, c->chunk, c->ns, c->ghost_cells,
@@ -257,19 +335,22 @@ int launch_fused(hftw_ctx* c, int src, int kernel) {
         if (c->tx == 64)
             hftw::step_tma_kernel<64, kNCW, PHYS><<<c->ctas, block, c->smem, c->stream>>>(
                 c->tm_e[src], c->tm_sf, c->tm_pb, e3(c, src), e3(c, src ^ 1), sf2(c), pb2(c), d,
-                a);
+                a, h);
         else
             hftw::step_tma_kernel<32, kNCW, PHYS><<<c->ctas, block, c->smem, c->stream>>>(
                 c->tm_e[src], c->tm_sf, c->tm_pb, e3(c, src), e3(c, src ^ 1), sf2(c), pb2(c), d,
-                a);
+                a, h);
     } else {
-        const long long n = (c->g.nx + 2) * (c->g.ny + 2) * c->g.nz;
+        const long long n = (c->lnx + 2) * (c->lny + 2) * c->nz;
+        // a decomposed run's CTAs spin on neighbour flags, so they must all
+        // be resident: cap the grid at the SM count x a safe occupancy
+        const int blocks = c->dist ? std::min(grid_for(c, n), c->num_sms * 4) : grid_for(c, n);
         if (c->layout == HFTW_KIJ)
-            hftw::step_cell_kernel<true, PHYS><<<grid_for(c, n), 256, 0, c->stream>>>(
-                e3(c, src), e3(c, src ^ 1), sf2(c), pb2(c), d);
+            hftw::step_cell_kernel<true, PHYS><<<blocks, 256, 0, c->stream>>>(
+                e3(c, src), e3(c, src ^ 1), sf2(c), pb2(c), d, h);
         else
-            hftw::step_cell_kernel<false, PHYS><<<grid_for(c, n), 256, 0, c->stream>>>(
-                e3(c, src), e3(c, src ^ 1), sf2(c), pb2(c), d);
+            hftw::step_cell_kernel<false, PHYS><<<blocks, 256, 0, c->stream>>>(
+                e3(c, src), e3(c, src ^ 1), sf2(c), pb2(c), d, h);
     }
     CUDA_TRY(c, cudaGetLastError());
     return HFTW_OK;
@@ -277,8 +358,8 @@ int launch_fused(hftw_ctx* c, int src, int kernel) {
 
 int launch_physics(hftw_ctx* c, int b, int mode) {
     Dom d = make_dom(c);
-    const long long cols = (c->g.nx + 2) * (c->g.ny + 2);
-    const long long n = cols * c->g.nz;
+    const long long cols = (c->lnx + 2) * (c->lny + 2);
+    const long long n = cols * c->nz;
     if (mode == 0) {
         if (c->layout == HFTW_KIJ)
             hftw::physics_kernel<true, true><<<grid_for(c, cols), 256, 0, c->stream>>>(
@@ -300,7 +381,7 @@ int launch_physics(hftw_ctx* c, int b, int mode) {
 
 // energy_u after a fused step is physics(previous energy); compute it in place
 // in the buffer that holds the previous energy (it is dead until the next step
-// overwrites it, so this is free of hazards).
+// overwrites it, so this is free of hazards; only owned cells are touched).
 int materialize_eu(hftw_ctx* c) {
     if (!c->eu_derived) return HFTW_OK;
     int rc = launch_physics(c, c->cur ^ 1, 1);
@@ -315,43 +396,62 @@ int check_ctx(hftw_ctx* c) {
     return HFTW_OK;
 }
 
-} // namespace
+// partition of n inner cells over p ranks (balanced; every rank >= 1 cell)
+long long part_lo(long long n, int p, int r) { return 1 + (long long)r * n / p; }
+long long part_hi(long long n, int p, int r) { return (long long)(r + 1) * n / p; }
 
-extern "C" {
-
-int hftw_abi_version(void) { return HFTW_ABI_VERSION; }
-
-int hftw_validate(const hftw_grid* g, char* msg, size_t cap) {
-    // hft::validate, weather.cpp:24-41 (messages verbatim, one per line)
-    if (msg && cap) msg[0] = 0;
-    if (!g) return fail(nullptr, HFTW_EINVAL, "null grid");
-    std::string out;
-    bool ok = true;
-    if (g->nx < 2 || g->ny < 2 || g->nz < 2) {
-        out += "<config>: error: grid extents must be at least 2 in every dimension\n";
-        ok = false;
-    }
-    if (!(g->diffusion_velocity <= 1.0 / 6.0) || g->diffusion_velocity < 0.0) {
-        out += "<config>: error: diffusion velocity must lie in [0, 1/6] so the center "
-               "coefficient stays nonnegative\n";
-        ok = false;
-    }
-    if (g->timestep <= 0.0 || g->output_timestep <= 0.0) {
-        out += "<config>: error: timestep and output timestep must be positive\n";
-        ok = false;
-    }
-    if (ok && (g->nx > (1LL << 30) || g->ny > (1LL << 30) || g->nz > (1LL << 30)))
-        out += "<config>: error: extents beyond 2^30 are not supported by the device store\n",
-            ok = false;
-    if (msg && cap) std::snprintf(msg, cap, "%s", out.c_str());
-    if (!ok) {
-        g_err = out;
-        return HFTW_EINVAL;
-    }
+int make_plan(const hftw_grid* g, int px, int py, int rank, hftw_plan* o) {
+    if (px < 1 || py < 1 || rank < 0 || rank >= px * py)
+        return fail(nullptr, HFTW_EINVAL, "bad decomposition %dx%d rank %d", px, py, rank);
+    if (px > g->nx || py > g->ny)
+        return fail(nullptr, HFTW_EINVAL, "decomposition %dx%d finer than the %lldx%lld interior",
+                    px, py, (long long)g->nx, (long long)g->ny);
+    hftw_plan p{};
+    p.px = px;
+    p.py = py;
+    p.rank = rank;
+    p.rx = rank % px;
+    p.ry = rank / px;
+    const long long ilo = part_lo(g->nx, px, p.rx), ihi = part_hi(g->nx, px, p.rx);
+    const long long jlo = part_lo(g->ny, py, p.ry), jhi = part_hi(g->ny, py, p.ry);
+    p.gi0 = ilo - 1;
+    p.gj0 = jlo - 1;
+    p.lnx = ihi - ilo + 1;
+    p.lny = jhi - jlo + 1;
+    p.own_w = p.rx == 0;
+    p.own_e = p.rx == px - 1;
+    p.own_s = p.ry == 0;
+    p.own_n = p.ry == py - 1;
+    // cyclic partners of the ghost cells (weather.cpp:155-167): local with one
+    // rank in that direction, else the far halo slot the wrap neighbour fills
+    p.wfar = px == 1 ? (int)p.lnx : -1;
+    p.efar = px == 1 ? 1 : (int)p.lnx + 2;
+    p.sfar = py == 1 ? (int)p.lny : -1;
+    p.nfar = py == 1 ? 1 : (int)p.lny + 2;
+    const int rxw = (p.rx - 1 + px) % px, rxe = (p.rx + 1) % px;
+    const int rys = (p.ry - 1 + py) % py, ryn = (p.ry + 1) % py;
+    p.nbr[HFTW_W] = px > 1 ? p.ry * px + rxw : -1;
+    p.nbr[HFTW_E] = px > 1 ? p.ry * px + rxe : -1;
+    p.nbr[HFTW_S] = py > 1 ? rys * px + p.rx : -1;
+    p.nbr[HFTW_N] = py > 1 ? ryn * px + p.rx : -1;
+    // where my faces land in the neighbour (its local coordinates)
+    const long long lnx_w = part_hi(g->nx, px, rxw) - part_lo(g->nx, px, rxw) + 1;
+    const long long lny_s = part_hi(g->ny, py, rys) - part_lo(g->ny, py, rys) + 1;
+    p.send_slot[HFTW_W] = rxw == px - 1 ? (int)lnx_w + 2 : (int)lnx_w + 1; // its E / E-far slot
+    p.send_slot[HFTW_E] = rxe == 0 ? -1 : 0;                               // its W-far / W slot
+    p.send_slot[HFTW_S] = rys == py - 1 ? (int)lny_s + 2 : (int)lny_s + 1;
+    p.send_slot[HFTW_N] = ryn == 0 ? -1 : 0;
+    p.face_lo[HFTW_W] = p.face_lo[HFTW_E] = p.own_s ? 0 : 1;
+    p.face_hi[HFTW_W] = p.face_hi[HFTW_E] = p.own_n ? p.lny + 1 : p.lny;
+    p.face_lo[HFTW_S] = p.face_lo[HFTW_N] = 1;
+    p.face_hi[HFTW_S] = p.face_hi[HFTW_N] = p.lnx;
+    *o = p;
     return HFTW_OK;
 }
 
-int hftw_create(const hftw_grid* g, int layout, int device, hftw_ctx** out) {
+// Allocate and lay out the local store (shared by create and create_dist).
+int create_common(const hftw_grid* g, int layout, int device, const hftw_plan& plan, bool dist,
+                  hftw_ctx** out) {
     if (!out) return fail(nullptr, HFTW_EINVAL, "null output pointer");
     *out = nullptr;
     char msg[512];
@@ -361,26 +461,33 @@ int hftw_create(const hftw_grid* g, int layout, int device, hftw_ctx** out) {
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
         cudaGetLastError();
-        return fail(nullptr, HFTW_ECUDA, "no CUDA device available (the B200 path has no CPU fallback)");
+        return fail(nullptr, HFTW_ECUDA,
+                    "no CUDA device available (the B200 path has no CPU fallback)");
     }
     if (device < 0 || device >= ndev) return fail(nullptr, HFTW_EINVAL, "bad device %d", device);
 
     hftw_ctx* c = new hftw_ctx();
     c->g = *g;
+    c->plan = plan;
+    c->dist = dist;
     c->layout = layout;
     c->device = device;
+    c->lnx = plan.lnx;
+    c->lny = plan.lny;
+    c->nz = g->nz;
     auto bail = [&](int rc) {
         g_err = c->err;
         hftw_destroy(c);
         return rc;
     };
-    if (cudaSetDevice(device) != cudaSuccess) return bail(fail(c, HFTW_ECUDA, "cudaSetDevice failed"));
+    if (cudaSetDevice(device) != cudaSuccess)
+        return bail(fail(c, HFTW_ECUDA, "cudaSetDevice failed"));
     cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
         return bail(fail(c, HFTW_ECUDA, "stream creation failed"));
     c->own_stream = true;
 
-    const long long nx = g->nx, ny = g->ny, nz = g->nz;
+    const long long nx = c->lnx, ny = c->lny, nz = c->nz;
     if (layout == HFTW_IJK) {
         // rows hold i = -1 .. nx+2 with logical i = 1 at element 32 (256 B)
         c->Pi = ((kFrontPad + nx + 3) + 31) / 32 * 32;
@@ -411,9 +518,14 @@ int hftw_create(const hftw_grid* g, int layout, int device, hftw_ctx** out) {
     if (cudaMalloc(&c->sf, c->n2 * sizeof(double)) != cudaSuccess ||
         cudaMalloc(&c->pb, c->n2 * sizeof(double)) != cudaSuccess)
         return bail(fail(c, HFTW_ENOMEM, "cudaMalloc of 2D fields failed"));
+    if (cudaMalloc(&c->flags, 4 * sizeof(unsigned long long)) != cudaSuccess ||
+        cudaMalloc(&c->done, sizeof(int)) != cudaSuccess)
+        return bail(fail(c, HFTW_ENOMEM, "cudaMalloc of halo flags failed"));
     for (int b = 0; b < 2; ++b) cudaMemsetAsync(c->buf[b], 0, c->n3 * sizeof(double), c->stream);
     cudaMemsetAsync(c->sf, 0, c->n2 * sizeof(double), c->stream);
     cudaMemsetAsync(c->pb, 0, c->n2 * sizeof(double), c->stream);
+    cudaMemsetAsync(c->flags, 0, 4 * sizeof(unsigned long long), c->stream);
+    cudaMemsetAsync(c->done, 0, sizeof(int), c->stream);
     if (cudaStreamSynchronize(c->stream) != cudaSuccess)
         return bail(fail(c, HFTW_ECUDA, "initial memset failed"));
     int rc = setup_tma(c);
@@ -422,16 +534,167 @@ int hftw_create(const hftw_grid* g, int layout, int device, hftw_ctx** out) {
     return HFTW_OK;
 }
 
+// Host <-> device copy of the OWNED part of a 3D field.  `host` is the
+// GLOBAL logical column-major array; dev_logical points at local (0,0,1).
+int copy_3d(hftw_ctx* c, double* dev_logical, double* host, bool h2d) {
+    const long long gnx = c->g.nx, gny = c->g.ny, nz = c->nz;
+    const Box o = owned_box(c);
+    const long long ni = o.i1 - o.i0 + 1, nj = o.j1 - o.j0 + 1;
+    const long long gi = c->plan.gi0 + o.i0, gj = c->plan.gj0 + o.j0; // global start
+    cudaPitchedPtr hp = make_cudaPitchedPtr(host, (size_t)(gnx + 2) * 8, (size_t)(gnx + 2),
+                                            (size_t)(gny + 2));
+    cudaPos hpos = make_cudaPos((size_t)gi * 8, (size_t)gj, 0);
+    if (c->layout == HFTW_IJK) {
+        cudaMemcpy3DParms p{};
+        cudaPitchedPtr dp = make_cudaPitchedPtr(dev_logical - c->off3, (size_t)c->Pi * 8,
+                                                (size_t)c->Pi, (size_t)c->Rows);
+        cudaPos dpos = make_cudaPos((size_t)(kFrontPad + o.i0) * 8, (size_t)(1 + o.j0), 0);
+        p.extent = make_cudaExtent((size_t)ni * 8, (size_t)nj, (size_t)nz);
+        if (h2d) {
+            p.srcPtr = hp;
+            p.srcPos = hpos;
+            p.dstPtr = dp;
+            p.dstPos = dpos;
+            p.kind = cudaMemcpyHostToDevice;
+        } else {
+            p.srcPtr = dp;
+            p.srcPos = dpos;
+            p.dstPtr = hp;
+            p.dstPos = hpos;
+            p.kind = cudaMemcpyDeviceToHost;
+        }
+        CUDA_TRY(c, cudaMemcpy3DAsync(&p, c->stream));
+        return HFTW_OK;
+    }
+    // KIJ: the owned box goes through a dense device staging box
+    const long long n = ni * nj * nz;
+    if (c->staging_n < (size_t)n) {
+        if (c->staging) cudaFree(c->staging);
+        c->staging = nullptr;
+        CUDA_TRY(c, cudaMalloc(&c->staging, (size_t)n * sizeof(double)));
+        c->staging_n = (size_t)n;
+    }
+    cudaMemcpy3DParms p{};
+    cudaPitchedPtr sp = make_cudaPitchedPtr(c->staging, (size_t)ni * 8, (size_t)ni, (size_t)nj);
+    p.extent = make_cudaExtent((size_t)ni * 8, (size_t)nj, (size_t)nz);
+    double* box = dev_logical + o.i0 * c->si + o.j0 * c->sj;
+    if (h2d) {
+        p.srcPtr = hp;
+        p.srcPos = hpos;
+        p.dstPtr = sp;
+        p.kind = cudaMemcpyHostToDevice;
+        CUDA_TRY(c, cudaMemcpy3DAsync(&p, c->stream));
+        hftw::relayout_kernel<true><<<grid_for(c, n), 256, 0, c->stream>>>(
+            c->staging, box, ni, nj, nz, c->si, c->sj, c->sk);
+        CUDA_TRY(c, cudaGetLastError());
+    } else {
+        hftw::relayout_kernel<false><<<grid_for(c, n), 256, 0, c->stream>>>(
+            box, c->staging, ni, nj, nz, c->si, c->sj, c->sk);
+        CUDA_TRY(c, cudaGetLastError());
+        p.srcPtr = sp;
+        p.dstPtr = hp;
+        p.dstPos = hpos;
+        p.kind = cudaMemcpyDeviceToHost;
+        CUDA_TRY(c, cudaMemcpy3DAsync(&p, c->stream));
+    }
+    return HFTW_OK;
+}
+
+int copy_2d(hftw_ctx* c, double* dev_logical, double* host, bool h2d) {
+    const long long gnx = c->g.nx;
+    const Box o = owned_box(c);
+    const long long ni = o.i1 - o.i0 + 1, nj = o.j1 - o.j0 + 1;
+    const long long gi = c->plan.gi0 + o.i0, gj = c->plan.gj0 + o.j0;
+    double* h = host + gi + gj * (gnx + 2);
+    double* d = dev_logical + o.i0 + o.j0 * c->s2j;
+    const size_t hp = (size_t)(gnx + 2) * 8, dp = (size_t)c->s2j * 8, w = (size_t)ni * 8;
+    if (h2d)
+        CUDA_TRY(c, cudaMemcpy2DAsync(d, dp, h, hp, w, (size_t)nj, cudaMemcpyHostToDevice,
+                                      c->stream));
+    else
+        CUDA_TRY(c, cudaMemcpy2DAsync(h, hp, d, dp, w, (size_t)nj, cudaMemcpyDeviceToHost,
+                                      c->stream));
+    return HFTW_OK;
+}
+
+} // namespace
+
+extern "C" {
+
+int hftw_abi_version(void) { return HFTW_ABI_VERSION; }
+
+int hftw_validate(const hftw_grid* g, char* msg, size_t cap) {
+    // hft::validate, weather.cpp:24-41 (messages verbatim, one per line)
+    if (msg && cap) msg[0] = 0;
+    if (!g) return fail(nullptr, HFTW_EINVAL, "null grid");
+    std::string out;
+    bool ok = true;
+    if (g->nx < 2 || g->ny < 2 || g->nz < 2) {
+        out += "<config>: error: grid extents must be at least 2 in every dimension\n";
+        ok = false;
+    }
+    if (!(g->diffusion_velocity <= 1.0 / 6.0) || g->diffusion_velocity < 0.0) {
+        out += "<config>: error: diffusion velocity must lie in [0, 1/6] so the center "
+               "coefficient stays nonnegative\n";
+        ok = false;
+    }
+    if (g->timestep <= 0.0 || g->output_timestep <= 0.0) {
+        out += "<config>: error: timestep and output timestep must be positive\n";
+        ok = false;
+    }
+    if (ok && (g->nx > (1LL << 30) || g->ny > (1LL << 30) || g->nz > (1LL << 30))) {
+        out += "<config>: error: extents beyond 2^30 are not supported by the device store\n";
+        ok = false;
+    }
+    if (msg && cap) std::snprintf(msg, cap, "%s", out.c_str());
+    if (!ok) {
+        g_err = out;
+        return HFTW_EINVAL;
+    }
+    return HFTW_OK;
+}
+
+int hftw_plan_rank(const hftw_grid* g, int px, int py, int rank, hftw_plan* out) {
+    if (!g || !out) return fail(nullptr, HFTW_EINVAL, "null argument");
+    char msg[512];
+    if (hftw_validate(g, msg, sizeof msg) != HFTW_OK) return fail(nullptr, HFTW_EINVAL, "%s", msg);
+    return make_plan(g, px, py, rank, out);
+}
+
+int hftw_create(const hftw_grid* g, int layout, int device, hftw_ctx** out) {
+    if (!g) return fail(nullptr, HFTW_EINVAL, "null grid");
+    hftw_plan p{};
+    char msg[512];
+    if (hftw_validate(g, msg, sizeof msg) != HFTW_OK) return fail(nullptr, HFTW_EINVAL, "%s", msg);
+    int rc = make_plan(g, 1, 1, 0, &p);
+    if (rc) return rc;
+    return create_common(g, layout, device, p, false, out);
+}
+
+int hftw_create_dist(const hftw_grid* g, int layout, int device, int px, int py, int rank,
+                     hftw_ctx** out) {
+    if (!g) return fail(nullptr, HFTW_EINVAL, "null grid");
+    hftw_plan p{};
+    int rc = hftw_plan_rank(g, px, py, rank, &p);
+    if (rc) return rc;
+    rc = create_common(g, layout, device, p, px * py > 1, out);
+    if (rc == HFTW_OK && (*out)->dist) (*out)->halo_dirty = true;
+    return rc;
+}
+
 void hftw_destroy(hftw_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
     for (int b = 0; b < 2; ++b)
         if (c->buf[b]) cudaFree(c->buf[b]);
     if (c->sf) cudaFree(c->sf);
     if (c->pb) cudaFree(c->pb);
     if (c->staging) cudaFree(c->staging);
     if (c->d_sched) cudaFree(c->d_sched);
+    if (c->flags) cudaFree(c->flags);
+    if (c->done) cudaFree(c->done);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -442,81 +705,30 @@ int hftw_init(hftw_ctx* c) {
     for (int b = 0; b < 2; ++b)
         CUDA_TRY(c, cudaMemsetAsync(c->buf[b], 0, c->n3 * sizeof(double), c->stream));
     Dom d = make_dom(c);
-    const long long n = (c->g.nx + 2) * (c->g.ny + 2) * c->g.nz;
+    const long long n = (c->lnx + 2) * (c->lny + 2) * c->nz;
+    const int gnx = (int)c->g.nx, gny = (int)c->g.ny, gnz = (int)c->g.nz;
+    const int gi0 = (int)c->plan.gi0, gj0 = (int)c->plan.gj0;
     if (c->layout == HFTW_KIJ)
         hftw::init_kernel<true><<<grid_for(c, n), 256, 0, c->stream>>>(
-            e3(c, c->cur), sf2(c), pb2(c), d, d.nx, d.ny, d.nz, 0, 0, c->g.surf_energy,
+            e3(c, c->cur), sf2(c), pb2(c), d, gnx, gny, gnz, gi0, gj0, c->g.surf_energy,
             c->g.pbl_energy);
     else
         hftw::init_kernel<false><<<grid_for(c, n), 256, 0, c->stream>>>(
-            e3(c, c->cur), sf2(c), pb2(c), d, d.nx, d.ny, d.nz, 0, 0, c->g.surf_energy,
+            e3(c, c->cur), sf2(c), pb2(c), d, gnx, gny, gnz, gi0, gj0, c->g.surf_energy,
             c->g.pbl_energy);
     CUDA_TRY(c, cudaGetLastError());
     if (c->d_sched) CUDA_TRY(c, cudaMemsetAsync(c->d_sched, 0, 2 * sizeof(int), c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     c->eu_derived = false; // energy_u is all zeros (weather.cpp:82)
-    c->initialized = true;
-    return HFTW_OK;
-}
-
-static int copy_3d(hftw_ctx* c, double* dev_logical, double* host, bool h2d) {
-    const long long nx = c->g.nx, ny = c->g.ny, nz = c->g.nz;
-    if (c->layout == HFTW_IJK) {
-        cudaMemcpy3DParms p{};
-        cudaPitchedPtr hp = make_cudaPitchedPtr(host, (size_t)(nx + 2) * 8, (size_t)(nx + 2),
-                                                (size_t)(ny + 2));
-        // dev_logical points at logical (0,0,1); describe the allocation around it
-        cudaPitchedPtr dp = make_cudaPitchedPtr(dev_logical - c->off3, (size_t)c->Pi * 8,
-                                                (size_t)c->Pi, (size_t)c->Rows);
-        cudaPos dpos = make_cudaPos((size_t)(c->off3 % c->Pi) * 8, (size_t)(c->off3 / c->Pi), 0);
-        p.extent = make_cudaExtent((size_t)(nx + 2) * 8, (size_t)(ny + 2), (size_t)nz);
-        if (h2d) {
-            p.srcPtr = hp;
-            p.dstPtr = dp;
-            p.dstPos = dpos;
-            p.kind = cudaMemcpyHostToDevice;
-        } else {
-            p.srcPtr = dp;
-            p.srcPos = dpos;
-            p.dstPtr = hp;
-            p.kind = cudaMemcpyDeviceToHost;
-        }
-        CUDA_TRY(c, cudaMemcpy3DAsync(&p, c->stream));
-        return HFTW_OK;
-    }
-    const long long n = (nx + 2) * (ny + 2) * nz;
-    if (!c->staging) CUDA_TRY(c, cudaMalloc(&c->staging, (size_t)n * sizeof(double)));
-    if (h2d) {
-        CUDA_TRY(c, cudaMemcpyAsync(c->staging, host, (size_t)n * 8, cudaMemcpyHostToDevice,
-                                    c->stream));
-        hftw::relayout_kernel<true><<<grid_for(c, n), 256, 0, c->stream>>>(
-            c->staging, dev_logical, nx + 2, ny + 2, nz, c->si, c->sj, c->sk);
-        CUDA_TRY(c, cudaGetLastError());
-    } else {
-        hftw::relayout_kernel<false><<<grid_for(c, n), 256, 0, c->stream>>>(
-            dev_logical, c->staging, nx + 2, ny + 2, nz, c->si, c->sj, c->sk);
-        CUDA_TRY(c, cudaGetLastError());
-        CUDA_TRY(c, cudaMemcpyAsync(host, c->staging, (size_t)n * 8, cudaMemcpyDeviceToHost,
-                                    c->stream));
-    }
-    return HFTW_OK;
-}
-
-static int copy_2d(hftw_ctx* c, double* dev_logical, double* host, bool h2d) {
-    const long long nx = c->g.nx, ny = c->g.ny;
-    const size_t w = (size_t)(nx + 2) * 8;
-    if (h2d)
-        CUDA_TRY(c, cudaMemcpy2DAsync(dev_logical, (size_t)c->s2j * 8, host, w, w,
-                                      (size_t)(ny + 2), cudaMemcpyHostToDevice, c->stream));
-    else
-        CUDA_TRY(c, cudaMemcpy2DAsync(host, w, dev_logical, (size_t)c->s2j * 8, w,
-                                      (size_t)(ny + 2), cudaMemcpyDeviceToHost, c->stream));
+    if (c->dist) c->halo_dirty = true;
     return HFTW_OK;
 }
 
 int hftw_upload(hftw_ctx* c, int field, const double* host) {
     int rc = check_ctx(c);
     if (rc) return rc;
-    if (!valid_field(field) || !host) return fail(c, HFTW_EINVAL, "bad field %d or null buffer", field);
+    if (!valid_field(field) || !host)
+        return fail(c, HFTW_EINVAL, "bad field %d or null buffer", field);
     double* h = const_cast<double*>(host);
     switch (field) {
     case HFTW_ENERGY:
@@ -535,14 +747,15 @@ int hftw_upload(hftw_ctx* c, int field, const double* host) {
     }
     if (rc) return rc;
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
-    c->initialized = true;
+    if (c->dist && field != HFTW_ENERGY_U) c->halo_dirty = true;
     return HFTW_OK;
 }
 
 int hftw_download(hftw_ctx* c, int field, double* host) {
     int rc = check_ctx(c);
     if (rc) return rc;
-    if (!valid_field(field) || !host) return fail(c, HFTW_EINVAL, "bad field %d or null buffer", field);
+    if (!valid_field(field) || !host)
+        return fail(c, HFTW_EINVAL, "bad field %d or null buffer", field);
     switch (field) {
     case HFTW_ENERGY:
         rc = copy_3d(c, e3(c, c->cur), host, false);
@@ -569,6 +782,14 @@ int hftw_step(hftw_ctx* c, int64_t nsteps) {
     if (nsteps < 0) return fail(c, HFTW_EINVAL, "steps must be nonnegative");
     if (nsteps == 0) return HFTW_OK;
     const int k = resolved_kernel(c);
+    if (c->dist) {
+        if (!c->connected) return fail(c, HFTW_ESTATE, "peers not connected (hftw_peer_connect)");
+        if (c->halo_dirty)
+            return fail(c, HFTW_ESTATE, "fields changed since the last hftw_exchange");
+        if (k == HFTW_KERNEL_SPLIT)
+            return fail(c, HFTW_EUNSUP, "the split (physics, then diffusion) kernel needs "
+                                        "post-physics halos; use a fused kernel when decomposed");
+    }
     for (int64_t s = 0; s < nsteps; ++s) {
         if (k == HFTW_KERNEL_SPLIT) {
             // the reference's structure: physics in place, then diffusion
@@ -582,6 +803,7 @@ int hftw_step(hftw_ctx* c, int64_t nsteps) {
             c->eu_derived = true;
         }
         c->cur ^= 1;
+        ++c->step_count;
     }
     return HFTW_OK;
 }
@@ -633,7 +855,8 @@ void* hftw_stream(hftw_ctx* c) { return c ? static_cast<void*>(c->stream) : null
 
 int hftw_set_kernel(hftw_ctx* c, int k) {
     if (!c) return fail(nullptr, HFTW_EINVAL, "null context");
-    if (k < HFTW_KERNEL_AUTO || k > HFTW_KERNEL_SPLIT) return fail(c, HFTW_EINVAL, "bad kernel %d", k);
+    if (k < HFTW_KERNEL_AUTO || k > HFTW_KERNEL_SPLIT)
+        return fail(c, HFTW_EINVAL, "bad kernel %d", k);
     if (k == HFTW_KERNEL_FUSED_TMA && !c->tma_ok)
         return fail(c, HFTW_EUNSUP, "TMA kernel needs the IJK layout and nz <= 256");
     c->kernel_req = k;
@@ -647,13 +870,17 @@ int hftw_physics(hftw_ctx* c, int mode) {
     if (rc) return rc;
     if (mode != 0 && mode != 1) return fail(c, HFTW_EINVAL, "bad physics mode %d", mode);
     if ((rc = materialize_eu(c))) return rc;
-    return launch_physics(c, c->cur, mode);
+    if ((rc = launch_physics(c, c->cur, mode))) return rc;
+    if (c->dist) c->halo_dirty = true;
+    return HFTW_OK;
 }
 
 int hftw_diffuse(hftw_ctx* c) {
     int rc = check_ctx(c);
     if (rc) return rc;
-    if ((rc = launch_fused<false>(c, c->cur, c->tma_ok ? HFTW_KERNEL_FUSED_TMA : HFTW_KERNEL_FUSED_CELL)))
+    if (c->dist) return fail(c, HFTW_EUNSUP, "diffusion-only sweeps are single-domain");
+    if ((rc = launch_fused<false>(c, c->cur,
+                                  c->tma_ok ? HFTW_KERNEL_FUSED_TMA : HFTW_KERNEL_FUSED_CELL)))
         return rc;
     c->eu_derived = false; // energy_u = the diffused input (swap semantics)
     c->cur ^= 1;
@@ -662,8 +889,10 @@ int hftw_diffuse(hftw_ctx* c) {
 
 double hftw_algorithmic_bytes(const hftw_ctx* c, int what) {
     if (!c) return 0.0;
-    const double cols = (double)(c->g.nx + 2) * (double)(c->g.ny + 2);
-    const double cells = cols * (double)c->g.nz;
+    // this context's stored cells (its subdomain's owned cells when decomposed)
+    const Box o = owned_box(c);
+    const double cols = (double)(o.i1 - o.i0 + 1) * (double)(o.j1 - o.j0 + 1);
+    const double cells = cols * (double)c->nz;
     switch (what) {
     case 0: return 16.0 * cells + 16.0 * cols; // read e, write u, read sf + pb
     case 1: return 16.0 * cells + 16.0 * cols; // physics: e read + write, sf + pb
@@ -692,6 +921,116 @@ int hftw_field_view(hftw_ctx* c, int field, void** dptr, int64_t strides[3]) {
     strides[0] = f3 ? c->si : 1;
     strides[1] = f3 ? c->sj : c->s2j;
     strides[2] = f3 ? c->sk : 0;
+    return HFTW_OK;
+}
+
+size_t hftw_peer_desc_size(void) { return sizeof(PeerDesc); }
+
+int hftw_peer_export(hftw_ctx* c, void* out) {
+    int rc = check_ctx(c);
+    if (rc) return rc;
+    if (!out) return fail(c, HFTW_EINVAL, "null descriptor buffer");
+    PeerDesc pd{};
+    for (int b = 0; b < 2; ++b) CUDA_TRY(c, cudaIpcGetMemHandle(&pd.buf[b], c->buf[b]));
+    CUDA_TRY(c, cudaIpcGetMemHandle(&pd.sf, c->sf));
+    CUDA_TRY(c, cudaIpcGetMemHandle(&pd.pb, c->pb));
+    CUDA_TRY(c, cudaIpcGetMemHandle(&pd.flags, c->flags));
+    pd.off3 = c->off3;
+    pd.off2 = c->off2;
+    pd.si = c->si;
+    pd.sj = c->sj;
+    pd.sk = c->sk;
+    pd.s2j = c->s2j;
+    pd.plan = c->plan;
+    pd.magic = kPeerMagic;
+    std::memcpy(out, &pd, sizeof pd);
+    return HFTW_OK;
+}
+
+int hftw_peer_connect(hftw_ctx* c, const void* all, int world) {
+    int rc = check_ctx(c);
+    if (rc) return rc;
+    if (!all || world != c->plan.px * c->plan.py)
+        return fail(c, HFTW_EINVAL, "need %d descriptors, got %d", c->plan.px * c->plan.py, world);
+    const PeerDesc* pds = static_cast<const PeerDesc*>(all);
+    std::map<int, PeerMap> opened; // a rank can be the neighbour in two directions
+    for (int d = 0; d < 4; ++d) {
+        const int r = c->plan.nbr[d];
+        if (r < 0) {
+            c->peer[d] = PeerMap{};
+            continue;
+        }
+        const PeerDesc& pd = pds[r];
+        if (pd.magic != kPeerMagic || pd.plan.rank != r)
+            return fail(c, HFTW_EINVAL, "descriptor %d is not rank %d's", r, r);
+        auto it = opened.find(r);
+        if (it == opened.end()) {
+            PeerMap m;
+            m.rank = r;
+            void* p = nullptr;
+            for (int b = 0; b < 2; ++b) {
+                CUDA_TRY(c, cudaIpcOpenMemHandle(&p, pd.buf[b], cudaIpcMemLazyEnablePeerAccess));
+                c->ipc_opened.push_back(p);
+                m.buf[b] = static_cast<double*>(p) + pd.off3;
+            }
+            CUDA_TRY(c, cudaIpcOpenMemHandle(&p, pd.sf, cudaIpcMemLazyEnablePeerAccess));
+            c->ipc_opened.push_back(p);
+            m.sf = static_cast<double*>(p) + pd.off2;
+            CUDA_TRY(c, cudaIpcOpenMemHandle(&p, pd.pb, cudaIpcMemLazyEnablePeerAccess));
+            c->ipc_opened.push_back(p);
+            m.pb = static_cast<double*>(p) + pd.off2;
+            CUDA_TRY(c, cudaIpcOpenMemHandle(&p, pd.flags, cudaIpcMemLazyEnablePeerAccess));
+            c->ipc_opened.push_back(p);
+            m.flags = static_cast<unsigned long long*>(p);
+            m.si = pd.si;
+            m.sj = pd.sj;
+            m.sk = pd.sk;
+            m.s2j = pd.s2j;
+            it = opened.emplace(r, m).first;
+        }
+        c->peer[d] = it->second;
+    }
+    c->connected = true;
+    return HFTW_OK;
+}
+
+int hftw_exchange(hftw_ctx* c) {
+    int rc = check_ctx(c);
+    if (rc) return rc;
+    if (!c->dist) {
+        c->halo_dirty = false;
+        return HFTW_OK;
+    }
+    if (!c->connected) return fail(c, HFTW_ESTATE, "peers not connected (hftw_peer_connect)");
+    Dom d = make_dom(c);
+    Halo h = make_halo(c, c->cur); // faces of the CURRENT field into the neighbours' current buffer
+    double* nsf[4] = {nullptr, nullptr, nullptr, nullptr};
+    double* npb[4] = {nullptr, nullptr, nullptr, nullptr};
+    long long n2j[4] = {0, 0, 0, 0};
+    for (int k = 0; k < 4; ++k)
+        if (c->peer[k].rank >= 0) {
+            nsf[k] = c->peer[k].sf;
+            npb[k] = c->peer[k].pb;
+            n2j[k] = c->peer[k].s2j;
+        }
+    const Box o = owned_box(c);
+    const long long n = (2 * (o.j1 - o.j0 + 1) + 2 * c->lnx) * c->nz;
+    hftw::exchange_kernel<<<grid_for(c, n), 256, 0, c->stream>>>(
+        e3(c, c->cur), sf2(c), pb2(c), d, h, nsf[0], nsf[1], nsf[2], nsf[3], npb[0], npb[1],
+        npb[2], npb[3], n2j[0], n2j[1], n2j[2], n2j[3], (int)o.j0, (int)o.j1);
+    CUDA_TRY(c, cudaGetLastError());
+    // a fresh epoch: step flags restart from zero on every rank
+    CUDA_TRY(c, cudaMemsetAsync(c->flags, 0, 4 * sizeof(unsigned long long), c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(c->done, 0, sizeof(int), c->stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    c->step_count = 0;
+    c->halo_dirty = false;
+    return HFTW_OK;
+}
+
+int hftw_get_plan(const hftw_ctx* c, hftw_plan* out) {
+    if (!c || !out) return fail(nullptr, HFTW_EINVAL, "null argument");
+    *out = c->plan;
     return HFTW_OK;
 }
 

@@ -185,12 +185,18 @@ class Context:
     reference keeps SimState on the host).  ``layout`` is "ijk" or "kij"."""
 
     def __init__(self, cfg: GridConfig, layout: str = "ijk", device: int = 0,
-                 kernel: str = "auto"):
+                 kernel: str = "auto", px: int = 1, py: int = 1, rank: int = 0):
+        """px x py > 1 creates rank `rank`'s subdomain of a decomposed run
+        (include/hftw.h, hftw_create_dist); see paper_1802_05839_b200.dist."""
         self.cfg = cfg
         self.layout = layout
         self._h = C.c_void_p()
-        check(lib().hftw_create(C.byref(cfg.to_c()), L.LAYOUTS[layout], device,
-                                C.byref(self._h)))
+        if px * py == 1:
+            check(lib().hftw_create(C.byref(cfg.to_c()), L.LAYOUTS[layout], device,
+                                    C.byref(self._h)))
+        else:
+            check(lib().hftw_create_dist(C.byref(cfg.to_c()), L.LAYOUTS[layout], device, px, py,
+                                         rank, C.byref(self._h)))
         if kernel != "auto":
             self.set_kernel(kernel)
 
@@ -270,11 +276,38 @@ class Context:
     def launches_per_step(self) -> int:
         return lib().hftw_launches_per_step(self._h)
 
+    # ---- decomposed runs -------------------------------------------------------
+    @property
+    def plan(self) -> dict:
+        p = L.hftw_plan()
+        self._chk(lib().hftw_get_plan(self._h, C.byref(p)))
+        return p.to_dict()
+
+    def export_peer(self) -> bytes:
+        n = lib().hftw_peer_desc_size()
+        buf = C.create_string_buffer(n)
+        self._chk(lib().hftw_peer_export(self._h, buf))
+        return buf.raw
+
+    def connect_peers(self, descs: List[bytes]) -> None:
+        blob = b"".join(descs)
+        self._chk(lib().hftw_peer_connect(self._h, C.c_char_p(blob), len(descs)))
+
+    def exchange(self) -> None:
+        self._chk(lib().hftw_exchange(self._h))
+
     def field_view(self, name: str) -> Tuple[int, Tuple[int, int, int]]:
         p = C.c_void_p()
         s = (C.c_int64 * 3)()
         self._chk(lib().hftw_field_view(self._h, L.FIELDS[name], C.byref(p), s))
         return p.value or 0, (s[0], s[1], s[2])
+
+
+def plan(cfg: GridConfig, px: int, py: int, rank: int) -> dict:
+    """hftw_plan_rank: rank's subdomain of a px x py decomposition (host only)."""
+    p = L.hftw_plan()
+    check(lib().hftw_plan_rank(C.byref(cfg.to_c()), px, py, rank, C.byref(p)))
+    return p.to_dict()
 
 
 def reference_init(cfg: GridConfig, st: SimState, device: int = 0) -> None:
