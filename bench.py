@@ -191,26 +191,48 @@ def run_reference_arm(args):
 # GPU arm
 # ---------------------------------------------------------------------------
 def run_ours(args):
-    import numpy as np
     import torch
     from paper_1802_05839_b200 import weather as W
+    from paper_1802_05839_b200.dist import DistSimulation, process_grid
 
     rank, world, local = dist_env()
+    ndev = max(1, torch.cuda.device_count())
+    device = local % ndev  # ranks > GPUs only when testing the protocol on one GPU
+    torch.cuda.set_device(device)
+    dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
+        # no data-path collective: gloo carries the one-time IPC descriptors,
+        # the barriers and the max-over-ranks of the timings
+        dist.init_process_group("gloo")
+        if args.workload != "full":
+            raise SystemExit("multi-GPU runs measure the full timestep only")
     grid, desc = WORKLOADS[args.workload]
     nx, ny, nz = grid
+    px, py = (args.px, args.py) if args.px else process_grid(world)
+    scaling = "weak" if world == 1 else args.scaling
+    if world > 1 and scaling == "weak":
+        nx, ny = nx * px, ny * py  # every GPU keeps an ASUCA-sized subdomain
+        desc = (f"full minimal-weather timestep, weak scaling: {nx}x{ny}x{nz} fp64 "
+                f"({px}x{py} ranks of ~1581x1301x58)")
+    elif world > 1:
+        desc = (f"full minimal-weather timestep on the ASUCA grid {nx}x{ny}x{nz} fp64, strong "
+                f"scaling over {px}x{py} B200 (I x J decomposition, in-kernel NVLink halo push)")
     cfg = W.GridConfig(nx=nx, ny=ny, nz=nz)
-    ctx = W.Context(cfg, layout=args.layout, device=local, kernel=args.kernel)
-    ctx.init()
-    stream = torch.cuda.ExternalStream(ctx.stream, device=local)
+    sim = None
+    if world == 1:
+        ctx = W.Context(cfg, layout=args.layout, device=device, kernel=args.kernel)
+        ctx.init()
+    else:
+        sim = DistSimulation(cfg, px, py, layout=args.layout, device=device, kernel=args.kernel)
+        sim.init()
+        ctx = sim.ctx
+    stream = torch.cuda.ExternalStream(ctx.stream, device=device)
     kernel_name = ctx.kernel
     flush = None
     if args.workload == "stencil":
         # 2 x 34 MB fits in L2: flush with a 256 MB write between sweeps
-        flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{device}")
         ctx.step(1)  # start from the state after one step (BASELINE configs[1])
 
     def one():
@@ -221,21 +243,20 @@ def run_ours(args):
         else:
             ctx.diffuse()
 
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
     for _ in range(args.warmup):
         one()
     ctx.sync()
-
-    def barrier():
-        if world > 1:
-            import torch.distributed as dist
-            dist.barrier()
 
     K = args.steps
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(K)]
     barrier()
     torch.cuda.synchronize()
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(device)
     with sampler:
         t_wall = time.perf_counter()
         with torch.cuda.stream(stream):
@@ -251,77 +272,100 @@ def run_ours(args):
     barrier()
     launch_ms = [a.elapsed_time(b) for a, b in evs]
     total_ms = evs[0][0].elapsed_time(evs[-1][1]) if flush is None else sum(launch_ms)
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([total_ms], device=f"cuda:{local}")
+    clocks = sampler.summary()
+    if dist is not None:
+        t = torch.tensor([total_ms], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
+        allc = [None] * world
+        dist.all_gather_object(allc, clocks)
+        mhz = [c["sm_mhz"] for c in allc if c["sm_mhz"]]
+        clocks = {"sm_mhz": min(mhz) if mhz else None, "sm_max_mhz": clocks["sm_max_mhz"],
+                  "reasons": sorted({r for c in allc for r in c["reasons"]}),
+                  "samples": sum(c["samples"] for c in allc), "per_rank_sm_mhz": mhz}
     ms_per_step = total_ms / K
     inner = nx * ny * nz
-    value = inner * world / (ms_per_step * 1e-3)
+    value = inner / (ms_per_step * 1e-3)
 
     what = {"full": "step", "physics": "physics", "stencil": "diffuse"}[args.workload]
-    alg_bytes = ctx.algorithmic_bytes(what)
+    alg_bytes = ctx.algorithmic_bytes(what)  # this rank's stored cells
     avg_launch_s = statistics.mean(launch_ms) * 1e-3
     peak, peak_src = peaks()
     achieved = alg_bytes / avg_launch_s / 1e9
-    traffic = ncu_traffic(args.workload, args.layout, kernel_name)
+    traffic = ncu_traffic(args.workload, args.layout, kernel_name) if world == 1 else None
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference_init initial condition; fp64 fields resident in HBM)",
-            "config": {"workload": desc, "grid": list(grid), "layout": args.layout,
+            "config": {"workload": desc, "grid": [nx, ny, nz], "layout": args.layout,
                        "kernel": kernel_name, "cells_counted": "inner nx*ny*nz per step",
                        "l2": ("flushed between sweeps (256 MB write)" if flush is not None else
                               "inputs larger than L2 (957 MB per field vs 126 MB L2)"),
-                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+                       "parallelism": (f"{px}x{py} I x J decomposition" if world > 1
+                                       else "single GPU")},
             "hbm_gbs": achieved,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "per": "GPU (rank 0)" if world > 1 else "GPU",
                          "algorithmic_bytes_per_launch": alg_bytes,
                          "avg_launch_ms": avg_launch_s * 1e3,
                          "paper_model_bytes_per_cell": {"m_sa=4": 32, "m_sa=10": 80}},
             "gpu_launches": K * (ctx.launches_per_step if args.workload == "full" else 1),
-            "clocks": sampler.summary(),
+            "clocks": clocks,
             "wall_s_timed_region": t_wall}
 
     if args.workload == "full" and not args.no_e2e:
-        line["e2e"] = e2e(ctx, cfg, args, stream, local, world)
+        if world > 1 and scaling == "weak":
+            line["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": None,
+                           "d2h_bytes_per_step": None,
+                           "why": "weak-scaled global grid too large for per-rank host buffers"}
+        else:
+            line["e2e"] = e2e(ctx, sim, cfg, args, stream, world)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, dt, kind, sample = cpu_reference_rate(grid, args.cpu_steps, args.workload)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": 1, "kind": kind,
                                 "sample": sample, "host_nproc": os.cpu_count()}
-    ctx.close()
+    if sim is not None:
+        sim.close()
+    else:
+        ctx.close()
     if rank == 0:
         print(json.dumps(line))
-    if world > 1:
-        import torch.distributed as dist
+    if dist is not None:
         dist.destroy_process_group()
     return 0
 
 
-def e2e(ctx, cfg, args, stream, local, world):
+def e2e(ctx, sim, cfg, args, stream, world):
     """Same metric through the reference-facing API with HOST buffers: each step
-    uploads the step's inputs (energy, energy_surf, energy_pbl) from pinned host
-    memory, runs hftw_step, and reads back the observable state (energy and
-    energy_u), i.e. the drop-in for hft::reference_step on a host SimState."""
+    uploads the step's inputs (energy, energy_surf, energy_pbl) from host memory,
+    runs hftw_step, and reads back the observable state (energy, energy_u) --
+    the drop-in for hft::reference_step on a host SimState.  Decomposed runs
+    move each rank's owned part and refill the halos (hftw_exchange)."""
     import torch
     n3 = (cfg.nx + 2) * (cfg.ny + 2) * cfg.nz
     n2 = (cfg.nx + 2) * (cfg.ny + 2)
-    bufs = {n: torch.empty(n3 if n in ("energy", "energy_u") else n2, dtype=torch.float64,
-                           pin_memory=True).numpy()
+    pinned = world == 1
+    mk = ((lambda n: torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()) if pinned
+          else (lambda n: __import__("numpy").empty(n)))
+    bufs = {n: mk(n3 if n in ("energy", "energy_u") else n2)
             for n in ("energy", "energy_u", "energy_surf", "energy_pbl")}
     for n in bufs:
         ctx.download(n, bufs[n])
     K = max(1, args.e2e_steps)
-    h2d = 8 * (n3 + 2 * n2)
-    d2h = 8 * (2 * n3)
+    own = ctx.algorithmic_bytes("physics") / 16.0  # owned stored cells + columns
+    cells = int(round(own * cfg.nz / (cfg.nz + 1)))
+    cols = int(round(own - cells))
+    h2d = 8 * (cells + 2 * cols)
+    d2h = 8 * (2 * cells)
 
     def one():
         ctx.upload("energy", bufs["energy"])
         ctx.upload("energy_surf", bufs["energy_surf"])
         ctx.upload("energy_pbl", bufs["energy_pbl"])
+        if sim is not None:
+            sim._exchange()
         ctx.step(1)
         ctx.download("energy", bufs["energy"])
         ctx.download("energy_u", bufs["energy_u"])
@@ -337,10 +381,16 @@ def e2e(ctx, cfg, args, stream, local, world):
     b.synchronize()
     wall = time.perf_counter() - t0
     ms = a.elapsed_time(b) / K
-    return {"value": cfg.nx * cfg.ny * cfg.nz * world / (ms * 1e-3), "unit": UNIT,
-            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": K,
+    if sim is not None:
+        t = torch.tensor([ms, wall], dtype=torch.float64)
+        sim.dist.all_reduce(t, op=sim.dist.ReduceOp.MAX)
+        ms, wall = float(t[0]), float(t[1])
+    return {"value": cfg.nx * cfg.ny * cfg.nz / (ms * 1e-3), "unit": UNIT,
+            "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h * world, "steps": K,
             "ms_per_step": ms, "wall_ms_per_step": wall / K * 1e3,
-            "api": "hftw_upload x3 + hftw_step(1) + hftw_download x2 (pinned host buffers)"}
+            "api": ("hftw_upload x3 + hftw_step(1) + hftw_download x2, pinned host buffers"
+                    if pinned else "per rank: hftw_upload x3 (owned part) + hftw_exchange + "
+                    "hftw_step(1) + hftw_download x2 (owned part), pageable host buffers")}
 
 
 def main():
@@ -357,6 +407,10 @@ def main():
     p.add_argument("--cpu-steps", type=int, default=16)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                   help="N>1: strong = ASUCA grid split over N GPUs; weak = ASUCA per GPU")
+    p.add_argument("--px", type=int, default=0, help="N>1: ranks along i (default: paper grid)")
+    p.add_argument("--py", type=int, default=0)
     args = p.parse_args()
     args.warmup = max(args.warmup, 3)  # timing rule: at least 3 warm-up steps
     if args.impl == "reference":
