@@ -100,10 +100,12 @@ _lib = None
 
 
 def lib(path: str = LIB) -> C.CDLL:
-    """Load libhftw.so (building it first when absent and nvcc exists)."""
+    """Load libhftw.so (building it first when absent and nvcc exists).
+    HFTW_LIBRARY overrides the path (tools/ experiment builds only)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = os.environ.get("HFTW_LIBRARY", path)
     if not os.path.exists(path):
         from ._build import build
         build()

@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -31,6 +32,12 @@ using hftw::Halo;
 namespace {
 
 thread_local std::string g_err; // errors of calls without a context
+
+// Tuning knobs for experiments (HFTW_TX=32|64, HFTW_NS=stages, HFTW_CHUNK=rows).
+int env_int(const char* name, int dflt) {
+    const char* v = std::getenv(name);
+    return (v && *v) ? std::atoi(v) : dflt;
+}
 
 constexpr int kFrontPad = 31; // IJK: logical i = 1 lands on a 256-byte boundary
 constexpr int kNCW = 16;      // consumer warps of the TMA kernel
@@ -238,12 +245,14 @@ int setup_tma(hftw_ctx* c) {
                                        c->device));
     const int nz = (int)c->nz;
     int tx = 0, ns = 0;
+    const int want_tx = env_int("HFTW_TX", 0), max_ns = env_int("HFTW_NS", 8);
     for (int cand : {64, 32}) {
+        if (want_tx && cand != want_tx) continue;
         hftw::SlabGeom G = hftw::slab_geom(cand, nz);
         int fit = (int)((smem_optin - 1024) / (G.stage + 20));
         if (fit >= 4) {
             tx = cand;
-            ns = std::min(fit, 8);
+            ns = std::max(4, std::min(fit, max_ns));
             break;
         }
     }
@@ -297,7 +306,14 @@ int setup_tma(hftw_ctx* c) {
     // themselves at the end of every launch.
     const long long nx = c->lnx, ny = c->lny;
     const int nstrips = (int)((nx + tx - 1) / tx);
-    c->chunk = (int)std::min<long long>(kChunk, ny);
+    // rows per unit: 32, or fewer when the grid would leave SMs idle
+    long long chunk = env_int("HFTW_CHUNK", 0);
+    if (chunk <= 0) {
+        chunk = kChunk;
+        const long long slots = (long long)per_sm * c->num_sms;
+        while (chunk > 4 && (long long)nstrips * ((ny + chunk - 1) / chunk) < 2 * slots) chunk /= 2;
+    }
+    c->chunk = (int)std::min<long long>(chunk, ny);
     c->nchunks = (int)((ny + c->chunk - 1) / c->chunk);
     const long long units = (long long)nstrips * c->nchunks;
     int ctas = (int)std::min<long long>((long long)per_sm * c->num_sms, units);

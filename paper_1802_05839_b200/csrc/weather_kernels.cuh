@@ -474,6 +474,95 @@ __device__ __forceinline__ double pin(double ev, double ri) {
     return PHYS ? dadd(ev, ri) : ev;
 }
 
+// One thread's share of one row in the TMA kernel: column i of the strip,
+// k in [kl, kh], with slabs j-1 (em), j (e0), j+1 (ep) in shared memory
+// (pointers already at the thread's slab column; +-1 are the i neighbours,
+// +-w the k neighbours).  A three-value register window carries P(k-1),
+// P(k), P(k+1); interior k run a branch-free loop, k = 1 / nz-1 / nz take
+// the boundary-aware path.
+struct ColumnRow {
+    const double *em, *e0, *ep;  // slab rows j-1, j, j+1
+    const double *Sm, *S0, *Sp;  // sf rows
+    const double *Bm, *B0, *Bp;  // pb rows
+    double* up;                  // u at (i, j, kl)
+    long long sk;
+    int w, kl, kh, nz;
+    double ri, tv, dv, c5, c6;
+    int i, j;
+};
+
+template <bool PHYS, bool PUSH>
+__device__ __forceinline__ void column_row(const ColumnRow& r, const Halo& h, const Dom& d) {
+    const int w = r.w, nz = r.nz;
+    const double ri = r.ri, tv = r.tv, dv = r.dv, c6 = r.c6;
+    auto Pc = [&](int kk) {
+        return phys<PHYS>(r.e0[(kk - 1) * w], kk, nz, r.S0[0], r.B0[0], ri, tv);
+    };
+    // boundary-aware cell (k = 1, nz-1, nz; any k is correct here)
+    auto edge = [&](int k, double pd, double pc, double& pn) {
+        pn = k < nz ? Pc(k + 1) : 0.0;
+        const int o = (k - 1) * w;
+        double s6 = dadd(phys<PHYS>(r.e0[o - 1], k, nz, r.S0[-1], r.B0[-1], ri, tv),
+                         phys<PHYS>(r.e0[o + 1], k, nz, r.S0[1], r.B0[1], ri, tv));
+        s6 = dadd(s6, phys<PHYS>(r.em[o], k, nz, r.Sm[0], r.Bm[0], ri, tv));
+        s6 = dadd(s6, phys<PHYS>(r.ep[o], k, nz, r.Sp[0], r.Bp[0], ri, tv));
+        if (k == 1) return dadd(dmul(r.c5, pc), dmul(dv, dadd(s6, pn)));  // weather.cpp:142-145
+        if (k == nz) return dadd(dmul(r.c5, pc), dmul(dv, dadd(s6, pd))); // weather.cpp:146-149
+        return dadd(dmul(c6, pc), dmul(dv, dadd(dadd(s6, pd), pn)));      // weather.cpp:134-137
+    };
+    double pd = r.kl > 1 ? Pc(r.kl - 1) : 0.0;
+    double pc = Pc(r.kl);
+    int k = r.kl;
+    for (; k <= r.kh && k < 2; ++k) { // k = 1
+        double pn;
+        const double out = edge(k, pd, pc, pn);
+        r.up[(long long)(k - r.kl) * r.sk] = out;
+        if (PUSH) halo_push(h, d, r.i, r.j, k, out);
+        pd = pc;
+        pc = pn;
+    }
+    const int kf = min(r.kh, nz - 2);
+    if (k <= kf) {
+        // interior k: weather.cpp:134-137 with P = e + ri for every operand
+        const double* p0 = r.e0 + (k - 1) * w;
+        const double* pm = r.em + (k - 1) * w;
+        const double* pp = r.ep + (k - 1) * w;
+        double* q = r.up + (long long)(k - r.kl) * r.sk;
+#pragma unroll 4
+        for (; k <= kf; ++k) {
+            const double pn = pin<PHYS>(p0[w], ri);
+            double s6 = dadd(pin<PHYS>(p0[-1], ri), pin<PHYS>(p0[1], ri));
+            s6 = dadd(s6, pin<PHYS>(pm[0], ri));
+            s6 = dadd(s6, pin<PHYS>(pp[0], ri));
+            s6 = dadd(dadd(s6, pd), pn);
+            double out = dadd(dmul(c6, pc), dmul(dv, s6));
+#if defined(HFTW_EXPERIMENT_COPY_ONLY) // tools/ experiment: memory path alone
+            out = p0[0];
+#endif
+#if !defined(HFTW_EXPERIMENT_NO_STORE)
+            *q = out;
+#else
+            if (out == -12345.678) *q = out; // keep the math live
+#endif
+            if (PUSH) halo_push(h, d, r.i, r.j, k, out);
+            q += r.sk;
+            p0 += w;
+            pm += w;
+            pp += w;
+            pd = pc;
+            pc = pn;
+        }
+    }
+    for (; k <= r.kh; ++k) { // k = nz-1, nz
+        double pn;
+        const double out = edge(k, pd, pc, pn);
+        r.up[(long long)(k - r.kl) * r.sk] = out;
+        if (PUSH) halo_push(h, d, r.i, r.j, k, out);
+        pd = pc;
+        pc = pn;
+    }
+}
+
 template <int TX, int NCW, bool PHYS>
 __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     step_tma_kernel(const __grid_constant__ CUtensorMap tm_e,
@@ -593,45 +682,12 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
                 const double* Bm = reinterpret_cast<const double*>(stm + G.e_bytes + G.r_bytes) + cc;
                 const double* B0 = reinterpret_cast<const double*>(st0 + G.e_bytes + G.r_bytes) + cc;
                 const double* Bp = reinterpret_cast<const double*>(stp + G.e_bytes + G.r_bytes) + cc;
-                // centre-column post-physics value at any k (boundary-aware)
-                auto Pc = [&](int kk) {
-                    return phys<PHYS>(e0[(kk - 1) * w], kk, nz, S0[0], B0[0], ri, tv);
-                };
                 double* up = u + (long long)(i0 + c) * d.si + (long long)j * d.sj +
                              (long long)(kl - 1) * d.sk;
-                double pd = kl > 1 ? Pc(kl - 1) : 0.0;
-                double pc = Pc(kl);
-                for (int k = kl; k <= kh; ++k) {
-                    const int o = (k - 1) * w;
-                    double out, pn;
-                    if (k >= 2 && k <= nz - 2) {
-                        // fast path: no boundary physics involved
-                        pn = pin<PHYS>(e0[o + w], ri);
-                        double s6 = dadd(pin<PHYS>(e0[o - 1], ri), pin<PHYS>(e0[o + 1], ri));
-                        s6 = dadd(s6, pin<PHYS>(em[o], ri));
-                        s6 = dadd(s6, pin<PHYS>(ep[o], ri));
-                        s6 = dadd(dadd(s6, pd), pn);
-                        out = dadd(dmul(c6, pc), dmul(dv, s6));
-                    } else {
-                        pn = k < nz ? Pc(k + 1) : 0.0;
-                        double s6 = dadd(phys<PHYS>(e0[o - 1], k, nz, S0[-1], B0[-1], ri, tv),
-                                         phys<PHYS>(e0[o + 1], k, nz, S0[1], B0[1], ri, tv));
-                        s6 = dadd(s6, phys<PHYS>(em[o], k, nz, Sm[0], Bm[0], ri, tv));
-                        s6 = dadd(s6, phys<PHYS>(ep[o], k, nz, Sp[0], Bp[0], ri, tv));
-                        if (k == 1) { // weather.cpp:142-145
-                            out = dadd(dmul(c5, pc), dmul(dv, dadd(s6, pn)));
-                        } else if (k == nz) { // weather.cpp:146-149
-                            out = dadd(dmul(c5, pc), dmul(dv, dadd(s6, pd)));
-                        } else { // weather.cpp:134-137
-                            out = dadd(dmul(c6, pc), dmul(dv, dadd(dadd(s6, pd), pn)));
-                        }
-                    }
-                    *up = out;
-                    up += d.sk;
-                    halo_push(h, d, i0 + c, j, k, out);
-                    pd = pc;
-                    pc = pn;
-                }
+                const ColumnRow r{em, e0, ep, Sm, S0, Sp, Bm, B0, Bp, up, d.sk, w, kl, kh, nz,
+                                  ri, tv, dv, c5, c6, i0 + c, j};
+                if (h.active) column_row<PHYS, true>(r, h, d);
+                else column_row<PHYS, false>(r, h, d);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[l0 % NS]);
