@@ -133,8 +133,10 @@ int hftw_get_kernel(const hftw_ctx* ctx);
 
 /* Phase 1 alone (weather.cpp:118-128): in-place column physics on ENERGY.
  * mode 0 = one column per thread with the k loop in registers (the
- * reference's emitted GPU mapping, emit_cuda.cpp:159-214), 1 = one cell per
- * thread along the fastest storage dimension.  Leaves ENERGY_U untouched. */
+ * reference's emitted GPU mapping, emit_cuda.cpp:159-214; coalesced in IJK,
+ * strided in KIJ), 1 = layout-aware mapping (IJK: i across threads along
+ * each (j,k) row; KIJ: one column per warp, lanes along k).  Leaves
+ * ENERGY_U untouched. */
 int hftw_physics(hftw_ctx* ctx, int mode);
 /* Phases 2-5 alone (weather.cpp:130-168): ENERGY <- diffusion(ENERGY), with
  * ENERGY_U receiving the previous ENERGY (the swap of weather.cpp:170). */
@@ -149,6 +151,21 @@ int hftw_launches_per_step(const hftw_ctx* ctx);
 /* Raw device view of a field for zero-copy interop: base pointer of logical
  * (i=0, j=0, k=1) and element strides (si, sj, sk); sk = 0 for 2D fields. */
 int hftw_field_view(hftw_ctx* ctx, int field, void** dptr, int64_t strides[3]);
+
+/* ---- output path ----------------------------------
+ * The corpus driver's time loop (fixtures/corpus/simple_weather.h90:74-108,
+ * driven by weather.cpp:364-376): time = start; loop { if modulo(time +
+ * 0.001, output_timestep) < 0.01 then write_data(energy, "energy", time);
+ * step; time = time + timestep; if time > end_time: stop }.  modulo is
+ * a - floor(a/p)*p (interpreter.cpp:109).  Each output is snapshotted on the
+ * device and copied to a pinned host ring on a separate stream while the
+ * following steps run; `write` receives the field as a logical column-major
+ * buffer that is valid only during the call (interpreter.hpp:68-69
+ * on_write_data).  Single-domain contexts only. */
+typedef void (*hftw_write_fn)(void* user, const char* tag, double time, const double* field);
+int hftw_simulate(hftw_ctx* ctx, double start_time, double end_time, double timestep,
+                  double output_timestep, hftw_write_fn write, void* user, int64_t* steps_done,
+                  int64_t* writes_done);
 
 /* ---- multi-GPU: 2D horizontal (I x J) decomposition, one process per GPU ----
  *

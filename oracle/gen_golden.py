@@ -122,7 +122,17 @@ def main():
             variants[f"{name}{'-reverse' if rev else ''}"] = {
                 "max_line_length": mll or 132, "bitwise_equal_to_reference": bool(same)}
 
+    # (8) the corpus driver's output cadence (simple_weather.h90:91-95): number
+    #     of write_data calls of the interpreted original for (steps, dt, out_dt)
+    writes = []
+    for steps, dt, odt in [(25, 0.1, 1.0), (10, 0.1, 1.0), (7, 0.25, 0.5), (30, 0.1, 0.3)]:
+        g = O.make_grid(timestep=dt, output_timestep=odt)
+        s, msg = ref.run_variant(1, g, steps, 0, False)
+        writes.append({"steps": steps, "timestep": dt, "output_timestep": odt,
+                       "write_data_calls": ref.last_write_calls, "ok": s is not None})
+
     meta = {"generator": "oracle/gen_golden.py", "full_cases": cases, "hashes": hashes,
+            "corpus_write_data": writes,
             "dumps": {"dump_energy_4x4x4_s2.txt": "energy after 2 steps, 4x4x4",
                       "dump_surf_4x4x4_s2.txt": "energy_surf, rank 2"},
             "variants_16x16x8_s10": variants}

@@ -168,7 +168,7 @@ class RefOracle:
         L.hftref_time_steps.restype = C.c_double
         L.hftref_run_variant.argtypes = [C.c_int, C.POINTER(Grid), C.c_longlong, C.c_int,
                                          C.c_int, C.c_char_p, D, D, D, D, C.c_char_p,
-                                         C.c_size_t]
+                                         C.c_size_t, C.POINTER(C.c_int)]
         LL = C.POINTER(C.c_longlong)
         L.hftref_compare_arrays.argtypes = [C.c_int, LL, LL, D, D, D, D, LL]
         L.hftref_unpermute.argtypes = [C.c_int, LL, LL, C.POINTER(C.c_int), D, D, LL, LL]
@@ -202,9 +202,12 @@ class RefOracle:
                     reverse: bool = False, corpus_dir: str = CORPUS_DIR):
         s = empty_state(g)
         buf = C.create_string_buffer(1 << 16)
+        wc = C.c_int(0)
         ok = self.lib.hftref_run_variant(variant, C.byref(g), n, max_line_length, int(reverse),
                                          corpus_dir.encode(), _p(s.energy), _p(s.energy_u),
-                                         _p(s.energy_surf), _p(s.energy_pbl), buf, 1 << 16)
+                                         _p(s.energy_surf), _p(s.energy_pbl), buf, 1 << 16,
+                                         C.byref(wc))
+        self.last_write_calls = wc.value
         return (s if ok else None), buf.value.decode()
 
     def compare_arrays(self, lo, hi, a: np.ndarray, b: np.ndarray):

@@ -109,7 +109,7 @@ double hftref_time_steps(const Grid* g, long long steps) {
 // avoids the split-before-expand failure, SURVEY.md finding 6).
 int hftref_run_variant(int variant, const Grid* g, long long steps, int max_line_length,
                        int reverse, const char* corpus_dir, double* e, double* eu, double* sf,
-                       double* pb, char* msg, size_t cap) {
+                       double* pb, char* msg, size_t cap, int* write_calls) {
     hft::Diagnostics d;
     std::vector<hft::LoadedSource> srcs;
     if (variant != 0) {
@@ -123,6 +123,7 @@ int hftref_run_variant(int variant, const Grid* g, long long steps, int max_line
                                          reverse ? hft::LaunchOrder::Reverse
                                                  : hft::LaunchOrder::Forward);
     copy_msg(d, msg, cap);
+    if (write_calls) *write_calls = r.write_data_calls;
     if (!r.ok) return 0;
     put_state(r.state, e, eu, sf, pb);
     return 1;

@@ -85,6 +85,8 @@ SIGNATURES = [
     ("hftw_algorithmic_bytes", C.c_double, [_P, C.c_int]),
     ("hftw_launches_per_step", C.c_int, [_P]),
     ("hftw_field_view", C.c_int, [_P, C.c_int, C.POINTER(_P), C.POINTER(C.c_int64)]),
+    ("hftw_simulate", C.c_int, [_P, C.c_double, C.c_double, C.c_double, C.c_double, _P, _P,
+                                C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     ("hftw_plan_rank", C.c_int, [C.POINTER(hftw_grid), C.c_int, C.c_int, C.c_int,
                                  C.POINTER(hftw_plan)]),
     ("hftw_create_dist", C.c_int, [C.POINTER(hftw_grid), C.c_int, C.c_int, C.c_int, C.c_int,
@@ -95,6 +97,9 @@ SIGNATURES = [
     ("hftw_exchange", C.c_int, [_P]),
     ("hftw_get_plan", C.c_int, [_P, C.POINTER(hftw_plan)]),
 ]
+
+# void (*)(void* user, const char* tag, double time, const double* field)
+WRITE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_char_p, C.c_double, C.POINTER(C.c_double))
 
 _lib = None
 

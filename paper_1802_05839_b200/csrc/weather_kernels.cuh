@@ -268,57 +268,79 @@ __global__ void exchange_kernel(const double* __restrict__ e, const double* __re
 }
 
 //------------------------------------------------------------------------------
-// Column physics alone, in place (weather.cpp:118-128).
-//  COLUMN: one (i,j) column per thread, k loop in registers -- the
-//          reference's emitted GPU mapping (hfk0_radiate + exchange,
-//          emit_cuda.cpp:159-214).  Coalesced in IJK, strided in KIJ.
-//  cell:   one cell per thread along the fastest storage dimension.
+// Column physics alone, in place (weather.cpp:118-128): BASELINE config (3).
+//  physics_column_kernel: one (i,j) column per thread with the k loop in
+//      registers -- the reference's emitted GPU mapping (hfk0_radiate +
+//      hfk0_exchange_heat_with_boundary, emit_cuda.cpp:159-214).  Coalesced in
+//      IJK; in KIJ neighbouring threads are a column apart (the paper's
+//      storage-order penalty).  Loads are batched 8 deep.
+//  physics_rows_kernel (IJK): one (j,k) row per block pass, i across threads.
+//  physics_kij_kernel (KIJ): one column per warp, lanes along k -- the
+//      KIJ-aware mapping.
 //------------------------------------------------------------------------------
-template <bool COLUMN, bool KFAST>
-__global__ void __launch_bounds__(256) physics_kernel(double* __restrict__ e,
-                                                      const double* __restrict__ sf,
-                                                      const double* __restrict__ pb, Dom d) {
+__global__ void __launch_bounds__(256) physics_column_kernel(double* __restrict__ e,
+                                                             const double* __restrict__ sf,
+                                                             const double* __restrict__ pb,
+                                                             Dom d) {
     Owned o = owned(d);
-    const long long ni = o.i1 - o.i0 + 1, nj = o.j1 - o.j0 + 1;
-    if (COLUMN) {
-        const long long n = ni * nj;
-        for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
-             t += (long long)gridDim.x * blockDim.x) {
-            int i = o.i0 + (int)(t % ni), j = o.j0 + (int)(t / ni);
-            double* col = e + i * d.si + j * d.sj;
-            for (int k = 1; k <= d.nz; ++k) {
-                double* p = col + (long long)(k - 1) * d.sk;
-                *p = dadd(*p, d.ri);
-            }
-            double s = __ldg(sf + i + j * d.s2j), b = __ldg(pb + i + j * d.s2j);
-            double v = col[0];
-            col[0] = dsub(v, dmul(d.tv, dsub(v, s)));
-            double* top = col + (long long)(d.nz - 1) * d.sk;
-            v = *top;
-            *top = dsub(v, dmul(d.tv, dsub(v, b)));
+    const int ni = o.i1 - o.i0 + 1, nj = o.j1 - o.j0 + 1;
+    const long long n = (long long)ni * nj;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+         t += (long long)gridDim.x * blockDim.x) {
+        const int i = o.i0 + (int)(t % ni), j = o.j0 + (int)(t / ni);
+        double* col = e + i * d.si + j * d.sj;
+        const double s = __ldg(sf + i + j * d.s2j), b = __ldg(pb + i + j * d.s2j);
+        for (int k0 = 1; k0 <= d.nz; k0 += 8) {
+            double v[8];
+#pragma unroll
+            for (int m = 0; m < 8; ++m)
+                if (k0 + m <= d.nz) v[m] = col[(long long)(k0 + m - 1) * d.sk];
+#pragma unroll
+            for (int m = 0; m < 8; ++m)
+                if (k0 + m <= d.nz)
+                    col[(long long)(k0 + m - 1) * d.sk] =
+                        phys<true>(v[m], k0 + m, d.nz, s, b, d.ri, d.tv);
         }
-    } else {
-        const long long nk = d.nz, n = ni * nj * nk;
-        for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
-             t += (long long)gridDim.x * blockDim.x) {
-            int i, j, k;
-            if (KFAST) {
-                k = 1 + (int)(t % nk);
-                long long r = t / nk;
-                i = o.i0 + (int)(r % ni);
-                j = o.j0 + (int)(r / ni);
-            } else {
-                i = o.i0 + (int)(t % ni);
-                long long r = t / ni;
-                j = o.j0 + (int)(r % nj);
-                k = 1 + (int)(r / nj);
-            }
-            double* p = e + i * d.si + j * d.sj + (long long)(k - 1) * d.sk;
+    }
+}
+
+__global__ void __launch_bounds__(256) physics_rows_kernel(double* __restrict__ e,
+                                                           const double* __restrict__ sf,
+                                                           const double* __restrict__ pb,
+                                                           Dom d) {
+    Owned o = owned(d);
+    const int ni = o.i1 - o.i0 + 1, nj = o.j1 - o.j0 + 1;
+    const long long rows = (long long)nj * d.nz;
+    for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
+        const int j = o.j0 + (int)(r % nj), k = 1 + (int)(r / nj);
+        double* row = e + j * d.sj + (long long)(k - 1) * d.sk;
+        const double* srow = sf + j * d.s2j;
+        const double* brow = pb + j * d.s2j;
+        for (int i = o.i0 + threadIdx.x; i <= o.i1; i += blockDim.x) {
             double sfv = 0.0, pbv = 0.0;
-            if (k == 1) sfv = __ldg(sf + i + j * d.s2j);
-            if (k == d.nz) pbv = __ldg(pb + i + j * d.s2j);
-            *p = phys<true>(*p, k, d.nz, sfv, pbv, d.ri, d.tv);
+            if (k == 1) sfv = __ldg(srow + i);
+            if (k == d.nz) pbv = __ldg(brow + i);
+            row[i] = phys<true>(row[i], k, d.nz, sfv, pbv, d.ri, d.tv);
         }
+    }
+}
+
+__global__ void __launch_bounds__(256) physics_kij_kernel(double* __restrict__ e,
+                                                          const double* __restrict__ sf,
+                                                          const double* __restrict__ pb,
+                                                          Dom d) {
+    Owned o = owned(d);
+    const int ni = o.i1 - o.i0 + 1, nj = o.j1 - o.j0 + 1;
+    const long long cols = (long long)ni * nj;
+    const int lane = threadIdx.x & 31;
+    const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long cw = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); cw < cols;
+         cw += warps) {
+        const int i = o.i0 + (int)(cw % ni), j = o.j0 + (int)(cw / ni);
+        double* col = e + i * d.si + j * d.sj; // k contiguous (sk == 1)
+        const double s = __ldg(sf + i + j * d.s2j), b = __ldg(pb + i + j * d.s2j);
+        for (int k = 1 + lane; k <= d.nz; k += 32)
+            col[k - 1] = phys<true>(col[k - 1], k, d.nz, s, b, d.ri, d.tv);
     }
 }
 
@@ -434,27 +456,59 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         : "memory");
 }
 
-// Shared-memory geometry of one pipeline stage.  A slab row spans logical
-// i0-2 .. i0+TX+1 (TX + 4 doubles): the TMA box must START on a 16-byte
-// boundary (an odd fp64 coordinate faults with an illegal instruction on
-// sm_100a), and the store side keeps i0 on a 256-byte boundary, so the box
-// begins one element before the i0-1 halo.  Column c of a slab row holds
-// logical i = i0 - 2 + c.
+// Shared-memory geometry of one pipeline stage.
+//  IJK: a slab row spans logical i0-2 .. i0+TX+1 (TX + 4 doubles) for every k
+//       ([k][i] in smem): the TMA box must START on a 16-byte boundary (an odd
+//       fp64 coordinate faults with an illegal instruction on sm_100a) and the
+//       stores keep i0 on a 256-byte boundary, so the box begins one element
+//       before the i0-1 halo.  Column c of a slab row holds logical i0-2+c.
+//  KIJ: a slab is the CONTIGUOUS block of columns i0-1 .. i0+TX, each Pk
+//       doubles of k ([i][k] in smem); Pk = 2 (mod 4) makes lanes that walk
+//       across columns at one k bank-conflict free for 64-bit accesses.
+//  Both: the sf/pb rows span i0-2 .. i0+TX+1.
 struct SlabGeom {
-    int w;          // TX + 4 doubles per slab row
+    int w;          // slab step between k and k+1 (doubles)
+    int is;         // slab step between i and i+1 (doubles)
     int e_bytes;    // slab bytes rounded to 128
     int r_bytes;    // one sf/pb row rounded to 128
     int stage;      // e + sf + pb
     int tx_bytes;   // bytes the TMA actually delivers per stage
+    int out_bytes;  // KIJ: one staged output row (TX x Pk), rounded to 128
 };
 __host__ __device__ inline SlabGeom slab_geom(int tx, int nz) {
     SlabGeom g;
     g.w = tx + 4;
+    g.is = 1;
     g.e_bytes = ((g.w * nz * 8) + 127) / 128 * 128;
-    g.r_bytes = ((g.w * 8) + 127) / 128 * 128;
+    g.r_bytes = (((tx + 4) * 8) + 127) / 128 * 128;
     g.stage = g.e_bytes + 2 * g.r_bytes;
-    g.tx_bytes = g.w * nz * 8 + 2 * g.w * 8;
+    g.tx_bytes = g.w * nz * 8 + 2 * (tx + 4) * 8;
+    g.out_bytes = 0;
     return g;
+}
+__host__ __device__ inline SlabGeom slab_geom_kij(int tx, int pk) {
+    SlabGeom g;
+    g.w = 1;
+    g.is = pk;
+    g.e_bytes = (((tx + 2) * pk * 8) + 127) / 128 * 128;
+    g.r_bytes = (((tx + 4) * 8) + 127) / 128 * 128;
+    g.stage = g.e_bytes + 2 * g.r_bytes;
+    g.tx_bytes = (tx + 2) * pk * 8 + 2 * (tx + 4) * 8;
+    g.out_bytes = ((tx * pk * 8) + 127) / 128 * 128;
+    return g;
+}
+
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+                 "r"(smem_u32(ssrc)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_all() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 struct TmaArgs {
@@ -464,6 +518,7 @@ struct TmaArgs {
     int nchunks;   // j-chunks of `chunk` rows over 1..ny
     int chunk;
     int ns;        // pipeline depth (stages)
+    int pk;        // KIJ column pitch (doubles)
     long long ghost_cells;
     int* sched;    // [0] next work unit, [1] CTAs finished (self-resetting)
 };
@@ -476,7 +531,7 @@ __device__ __forceinline__ double pin(double ev, double ri) {
 
 // One thread's share of one row in the TMA kernel: column i of the strip,
 // k in [kl, kh], with slabs j-1 (em), j (e0), j+1 (ep) in shared memory
-// (pointers already at the thread's slab column; +-1 are the i neighbours,
+// (pointers already at the thread's slab column; +-is are the i neighbours,
 // +-w the k neighbours).  A three-value register window carries P(k-1),
 // P(k), P(k+1); interior k run a branch-free loop, k = 1 / nz-1 / nz take
 // the boundary-aware path.
@@ -484,16 +539,17 @@ struct ColumnRow {
     const double *em, *e0, *ep;  // slab rows j-1, j, j+1
     const double *Sm, *S0, *Sp;  // sf rows
     const double *Bm, *B0, *Bp;  // pb rows
-    double* up;                  // u at (i, j, kl)
-    long long sk;
-    int w, kl, kh, nz;
+    double* up;                  // output at (i, j, kl): global (IJK) or smem staging (KIJ)
+    long long sk;                // output step between k and k+1
+    int w, is;                   // slab steps between k and k+1, i and i+1
+    int kl, kh, nz;
     double ri, tv, dv, c5, c6;
     int i, j;
 };
 
 template <bool PHYS, bool PUSH>
 __device__ __forceinline__ void column_row(const ColumnRow& r, const Halo& h, const Dom& d) {
-    const int w = r.w, nz = r.nz;
+    const int w = r.w, is = r.is, nz = r.nz;
     const double ri = r.ri, tv = r.tv, dv = r.dv, c6 = r.c6;
     auto Pc = [&](int kk) {
         return phys<PHYS>(r.e0[(kk - 1) * w], kk, nz, r.S0[0], r.B0[0], ri, tv);
@@ -502,8 +558,8 @@ __device__ __forceinline__ void column_row(const ColumnRow& r, const Halo& h, co
     auto edge = [&](int k, double pd, double pc, double& pn) {
         pn = k < nz ? Pc(k + 1) : 0.0;
         const int o = (k - 1) * w;
-        double s6 = dadd(phys<PHYS>(r.e0[o - 1], k, nz, r.S0[-1], r.B0[-1], ri, tv),
-                         phys<PHYS>(r.e0[o + 1], k, nz, r.S0[1], r.B0[1], ri, tv));
+        double s6 = dadd(phys<PHYS>(r.e0[o - is], k, nz, r.S0[-1], r.B0[-1], ri, tv),
+                         phys<PHYS>(r.e0[o + is], k, nz, r.S0[1], r.B0[1], ri, tv));
         s6 = dadd(s6, phys<PHYS>(r.em[o], k, nz, r.Sm[0], r.Bm[0], ri, tv));
         s6 = dadd(s6, phys<PHYS>(r.ep[o], k, nz, r.Sp[0], r.Bp[0], ri, tv));
         if (k == 1) return dadd(dmul(r.c5, pc), dmul(dv, dadd(s6, pn)));  // weather.cpp:142-145
@@ -531,7 +587,7 @@ __device__ __forceinline__ void column_row(const ColumnRow& r, const Halo& h, co
 #pragma unroll 4
         for (; k <= kf; ++k) {
             const double pn = pin<PHYS>(p0[w], ri);
-            double s6 = dadd(pin<PHYS>(p0[-1], ri), pin<PHYS>(p0[1], ri));
+            double s6 = dadd(pin<PHYS>(p0[-is], ri), pin<PHYS>(p0[is], ri));
             s6 = dadd(s6, pin<PHYS>(pm[0], ri));
             s6 = dadd(s6, pin<PHYS>(pp[0], ri));
             s6 = dadd(dadd(s6, pd), pn);
@@ -563,7 +619,7 @@ __device__ __forceinline__ void column_row(const ColumnRow& r, const Halo& h, co
     }
 }
 
-template <int TX, int NCW, bool PHYS>
+template <int TX, int NCW, bool PHYS, bool KIJ>
 __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     step_tma_kernel(const __grid_constant__ CUtensorMap tm_e,
                     const __grid_constant__ CUtensorMap tm_sf,
@@ -571,9 +627,10 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
                     double* __restrict__ u, const double* __restrict__ sf,
                     const double* __restrict__ pb, Dom d, TmaArgs a, Halo h) {
     extern __shared__ __align__(128) unsigned char smem[];
-    const SlabGeom G = slab_geom(TX, d.nz);
+    const SlabGeom G = KIJ ? slab_geom_kij(TX, a.pk) : slab_geom(TX, d.nz);
     const int NS = a.ns;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NS * G.stage);
+    unsigned char* outbuf = smem + (size_t)NS * G.stage; // KIJ: two staged output rows
+    uint64_t* full = reinterpret_cast<uint64_t*>(outbuf + 2 * (size_t)G.out_bytes);
     uint64_t* empty = full + NS;
     int* slot_unit = reinterpret_cast<int*>(empty + NS); // work unit of each staged slab
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -603,7 +660,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
                     const int ch = unit / a.nstrips, st = unit % a.nstrips;
                     ja = ch * a.chunk + 1;
                     jb = min(d.ny, ja + a.chunk - 1);
-                    ic = a.fp + 1 + st * TX - 2; // tensor coordinate of i0 - 2 (even)
+                    // IJK: tensor coordinate of i0 - 2 (even); KIJ: of column i0 - 1
+                    ic = KIJ ? 1 + st * TX : a.fp + 1 + st * TX - 2;
                     // a unit on the subdomain rim reads halo slots and pushes
                     // to that neighbour: wait until it finished the previous step
                     const int mask = (st == 0 ? 1 : 0) | (st == a.nstrips - 1 ? 2 : 0) |
@@ -623,9 +681,12 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
                     }
                     unsigned char* stg = smem + (size_t)slot * G.stage;
                     mbar_expect_tx(&full[slot], G.tx_bytes);
-                    tma_load_3d(stg, &tm_e, &full[slot], ic, a.jrow0 + jj, 0);
-                    tma_load_2d(stg + G.e_bytes, &tm_sf, &full[slot], ic, a.jrow0 + jj);
-                    tma_load_2d(stg + G.e_bytes + G.r_bytes, &tm_pb, &full[slot], ic,
+                    // KIJ sf/pb rows are i-contiguous: their (even) coordinate of i0 - 2
+                    const int ic2 = KIJ ? ic - 1 : ic;
+                    if (KIJ) tma_load_3d(stg, &tm_e, &full[slot], 0, ic, a.jrow0 + jj);
+                    else tma_load_3d(stg, &tm_e, &full[slot], ic, a.jrow0 + jj, 0);
+                    tma_load_2d(stg + G.e_bytes, &tm_sf, &full[slot], ic2, a.jrow0 + jj);
+                    tma_load_2d(stg + G.e_bytes + G.r_bytes, &tm_pb, &full[slot], ic2,
                                 a.jrow0 + jj);
                 }
                 if (stop) break;
@@ -650,7 +711,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     const int c = threadIdx.x % TX, g = threadIdx.x / TX;
     const int nz = d.nz;
     const int kl = 1 + (g * nz) / NKG, kh = ((g + 1) * nz) / NKG;
-    const int w = G.w, cc = c + 2; // slab column of cell i0 + c
+    const int w = G.w, cc = c + 2; // sf/pb (and IJK slab) column of cell i0 + c
+    const int eoff = KIJ ? (c + 1) * G.is : cc; // slab element of cell i0 + c at k = 1
     const double ri = d.ri, tv = d.tv, dv = d.dv, c5 = d.c5, c6 = d.c6;
 
     uint32_t L = 0; // load index of the first slab of the current unit
@@ -673,21 +735,38 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
                 const unsigned char* stm = smem + (size_t)(l0 % NS) * G.stage;
                 const unsigned char* st0 = smem + (size_t)(l1 % NS) * G.stage;
                 const unsigned char* stp = smem + (size_t)(l2 % NS) * G.stage;
-                const double* em = reinterpret_cast<const double*>(stm) + cc;
-                const double* e0 = reinterpret_cast<const double*>(st0) + cc;
-                const double* ep = reinterpret_cast<const double*>(stp) + cc;
+                const double* em = reinterpret_cast<const double*>(stm) + eoff;
+                const double* e0 = reinterpret_cast<const double*>(st0) + eoff;
+                const double* ep = reinterpret_cast<const double*>(stp) + eoff;
                 const double* Sm = reinterpret_cast<const double*>(stm + G.e_bytes) + cc;
                 const double* S0 = reinterpret_cast<const double*>(st0 + G.e_bytes) + cc;
                 const double* Sp = reinterpret_cast<const double*>(stp + G.e_bytes) + cc;
                 const double* Bm = reinterpret_cast<const double*>(stm + G.e_bytes + G.r_bytes) + cc;
                 const double* B0 = reinterpret_cast<const double*>(st0 + G.e_bytes + G.r_bytes) + cc;
                 const double* Bp = reinterpret_cast<const double*>(stp + G.e_bytes + G.r_bytes) + cc;
-                double* up = u + (long long)(i0 + c) * d.si + (long long)j * d.sj +
-                             (long long)(kl - 1) * d.sk;
-                const ColumnRow r{em, e0, ep, Sm, S0, Sp, Bm, B0, Bp, up, d.sk, w, kl, kh, nz,
-                                  ri, tv, dv, c5, c6, i0 + c, j};
+                // IJK: straight to global, 256-byte coalesced per warp.  KIJ: into
+                // the staged output row ([i][k], conflict free), bulk-stored below.
+                double* up = KIJ ? reinterpret_cast<double*>(outbuf + (size_t)(j & 1) * G.out_bytes) +
+                                       c * G.is + (kl - 1)
+                                 : u + (long long)(i0 + c) * d.si + (long long)j * d.sj +
+                                       (long long)(kl - 1) * d.sk;
+                const ColumnRow r{em, e0, ep, Sm, S0, Sp, Bm, B0, Bp, up, KIJ ? 1 : d.sk,
+                                  w, G.is, kl, kh, nz, ri, tv, dv, c5, c6, i0 + c, j};
                 if (h.active) column_row<PHYS, true>(r, h, d);
                 else column_row<PHYS, false>(r, h, d);
+            }
+            if (KIJ) {
+                // the row is staged: one thread stores it as ONE contiguous bulk
+                // copy (columns i0 .. i0+width-1 of row j are adjacent in KIJ)
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                if (threadIdx.x == 0) bulk_wait_read_all(); // row j-1's store has left its buffer
+                asm volatile("bar.sync 2, %0;" ::"r"(NCW * 32) : "memory");
+                if (threadIdx.x == 0) {
+                    const int width = min(TX, d.nx - i0 + 1);
+                    bulk_store(u + (long long)i0 * d.si + (long long)j * d.sj,
+                               outbuf + (size_t)(j & 1) * G.out_bytes,
+                               (uint32_t)(width * G.is * 8));
+                }
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[l0 % NS]);
@@ -730,6 +809,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
         }
     }
 
+    if (KIJ && threadIdx.x == 0) bulk_wait_all(); // staged rows have reached global memory
     // all consumer warps of this CTA are done: publish the step when last
     if (h.active) {
         asm volatile("bar.sync 1, %0;" ::"r"(NCW * 32) : "memory");

@@ -276,6 +276,31 @@ class Context:
     def launches_per_step(self) -> int:
         return lib().hftw_launches_per_step(self._h)
 
+    def simulate(self, start_time: float, end_time: float, timestep: float,
+                 output_timestep: float, write=None) -> Tuple[int, int]:
+        """The corpus driver's time loop (simple_weather.h90:74-108) on the
+        device.  ``write(tag, time, field)`` receives each output as a numpy
+        view of a pinned buffer, valid only during the call (copy to keep).
+        Returns (steps, writes)."""
+        n3 = (self.cfg.nx + 2) * (self.cfg.ny + 2) * self.cfg.nz
+        err = []
+
+        def tramp(_user, tag, time, field):
+            try:
+                arr = np.ctypeslib.as_array(field, shape=(n3,))
+                write(tag.decode(), time, arr)
+            except Exception as e:  # never unwind through C
+                err.append(e)
+
+        cb = L.WRITE_FN(tramp) if write is not None else C.cast(None, L.WRITE_FN)
+        steps, writes = C.c_int64(), C.c_int64()
+        self._chk(lib().hftw_simulate(self._h, start_time, end_time, timestep, output_timestep,
+                                      C.cast(cb, C.c_void_p), None, C.byref(steps),
+                                      C.byref(writes)))
+        if err:
+            raise err[0]
+        return steps.value, writes.value
+
     # ---- decomposed runs -------------------------------------------------------
     @property
     def plan(self) -> dict:
@@ -301,6 +326,18 @@ class Context:
         s = (C.c_int64 * 3)()
         self._chk(lib().hftw_field_view(self._h, L.FIELDS[name], C.byref(p), s))
         return p.value or 0, (s[0], s[1], s[2])
+
+
+def dump_writer(directory: str, cfg: GridConfig):
+    """A ``Context.simulate`` writer storing each output as ``energy_<time>.txt``
+    in the reference's dump format (weather.cpp:251-269)."""
+    import os
+
+    def write(tag: str, time: float, field: np.ndarray) -> None:
+        a = ArrayObject([(0, cfg.nx + 1), (0, cfg.ny + 1), (1, cfg.nz)], field.copy())
+        with open(os.path.join(directory, f"{tag}_{time:.6f}.txt"), "w") as f:
+            dump_field(f, a)
+    return write
 
 
 def plan(cfg: GridConfig, px: int, py: int, rank: int) -> dict:

@@ -18,7 +18,7 @@ pytestmark = pytest.mark.gpu
 
 TOL = 0.0  # bitwise
 LAYOUTS = ["ijk", "kij"]
-KERNELS = ["auto", "fused_cell", "split"]
+KERNELS = ["auto", "fused_cell", "split"]  # auto = the TMA kernel wherever it fits
 
 
 def cfg_of(d):
@@ -58,8 +58,9 @@ def test_golden_cases(golden, layout, kernel):
         assert_same(got, want, f"{name}/{layout}/{kernel}")
 
 
-def test_fused_tma_selected_for_ijk():
-    with W.Context(W.GridConfig(nx=100, ny=40, nz=58)) as ctx:
+@pytest.mark.parametrize("layout", LAYOUTS)
+def test_fused_tma_selected(layout):
+    with W.Context(W.GridConfig(nx=100, ny=40, nz=58), layout=layout) as ctx:
         assert ctx.kernel == "fused_tma"
         assert ctx.launches_per_step == 1
 
