@@ -315,6 +315,13 @@ def run_ours(args):
             "clocks": clocks,
             "wall_s_timed_region": t_wall}
 
+    if args.workload == "full":
+        # the paper's bandwidth model (perfmodel.cpp:141-154) on the measured B200
+        # entry, for the same grid: m_sa = 10 / 4 values per cell vs measured
+        from paper_1802_05839_b200 import perfmodel
+        lnx, lny = (ctx.plan["lnx"], ctx.plan["lny"]) if world > 1 else (nx, ny)
+        rep = perfmodel.b200_report(ms_per_step, lnx, lny, nz)  # per GPU
+        line["paper_model"] = {k: rep[k] for k in ("model_ms_per_step", "bw_d_GBps", "ra_d_GUPs")}
     if args.workload == "full" and not args.no_e2e:
         if world > 1 and scaling == "weak":
             line["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": None,
