@@ -231,8 +231,12 @@ def run_ours(args):
     kernel_name = ctx.kernel
     flush = None
     if args.workload == "stencil":
-        # 2 x 34 MB fits in L2: flush with a 256 MB write between sweeps
-        flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{device}")
+        # 2 x 34 MB fits in L2: flush with a 256 MB write between sweeps (on the
+        # context stream, outside the per-launch events)
+        flush = (lambda: ctx.flush_l2(256 << 20)) if args.flush == "hftw" else \
+            (lambda t=torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{device}"): t.add_(1))
+        if args.flush == "none":
+            flush = None
         ctx.step(1)  # start from the state after one step (BASELINE configs[1])
 
     def one():
@@ -262,7 +266,7 @@ def run_ours(args):
         with torch.cuda.stream(stream):
             for i in range(K):
                 if flush is not None:
-                    flush.add_(1)  # on `stream`: outside the per-launch events
+                    flush()  # on `stream`: outside the per-launch events
                 evs[i][0].record(stream)
                 one()
                 evs[i][1].record(stream)
@@ -300,8 +304,10 @@ def run_ours(args):
             "data": "synthetic (reference_init initial condition; fp64 fields resident in HBM)",
             "config": {"workload": desc, "grid": [nx, ny, nz], "layout": args.layout,
                        "kernel": kernel_name, "cells_counted": "inner nx*ny*nz per step",
-                       "l2": ("flushed between sweeps (256 MB write)" if flush is not None else
-                              "inputs larger than L2 (957 MB per field vs 126 MB L2)"),
+                       "l2": (f"flushed between sweeps (256 MB write, {args.flush})"
+                              if flush is not None else
+                              "inputs larger than L2 (957 MB per field vs 126 MB L2)"
+                              if args.workload != "stencil" else "NOT flushed (diagnostic)"),
                        "parallelism": (f"{px}x{py} I x J decomposition" if world > 1
                                        else "single GPU")},
             "hbm_gbs": achieved,
@@ -417,6 +423,8 @@ def main():
     p.add_argument("--scaling", choices=["strong", "weak"], default="strong",
                    help="N>1: strong = ASUCA grid split over N GPUs; weak = ASUCA per GPU")
     p.add_argument("--px", type=int, default=0, help="N>1: ranks along i (default: paper grid)")
+    p.add_argument("--flush", choices=["hftw", "torch", "none"], default="hftw",
+                   help="stencil workload: L2 flush between sweeps ('none' is diagnostic only)")
     p.add_argument("--py", type=int, default=0)
     args = p.parse_args()
     args.warmup = max(args.warmup, 3)  # timing rule: at least 3 warm-up steps

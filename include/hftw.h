@@ -142,6 +142,11 @@ int hftw_physics(hftw_ctx* ctx, int mode);
  * ENERGY_U receiving the previous ENERGY (the swap of weather.cpp:170). */
 int hftw_diffuse(hftw_ctx* ctx);
 
+/* Measurement hook: overwrite `bytes` of scratch device memory on the context
+ * stream (evicts the L2 between timed sweeps) with the same shared-memory
+ * configuration as the step kernel, so no carveout change is timed. */
+int hftw_flush_l2(hftw_ctx* ctx, size_t bytes);
+
 /* Algorithmic HBM bytes of one call: what = 0 full step, 1 physics, 2 diffusion
  * (16 B per stored cell + 16 B per column for a step). */
 double hftw_algorithmic_bytes(const hftw_ctx* ctx, int what);

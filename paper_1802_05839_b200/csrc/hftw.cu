@@ -125,6 +125,8 @@ struct hftw_ctx {
     };
     std::vector<OutSlot> out;
     cudaStream_t copy_stream = nullptr;
+    void* flush_buf = nullptr;
+    size_t flush_bytes = 0;
 
     std::string err;
 };
@@ -768,6 +770,7 @@ void hftw_destroy(hftw_ctx* c) {
         if (o.host) cudaFreeHost(o.host);
     }
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    if (c->flush_buf) cudaFree(c->flush_buf);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -994,6 +997,29 @@ int hftw_field_view(hftw_ctx* c, int field, void** dptr, int64_t strides[3]) {
     strides[0] = f3 ? c->si : 1;
     strides[1] = f3 ? c->sj : c->s2j;
     strides[2] = f3 ? c->sk : 0;
+    return HFTW_OK;
+}
+
+int hftw_flush_l2(hftw_ctx* c, size_t bytes) {
+    int rc = check_ctx(c);
+    if (rc) return rc;
+    bytes = (bytes + 31) / 32 * 32;
+    if (c->flush_bytes < bytes) {
+        if (c->flush_buf) cudaFree(c->flush_buf);
+        c->flush_buf = nullptr;
+        CUDA_TRY(c, cudaMalloc(&c->flush_buf, bytes));
+        c->flush_bytes = bytes;
+    }
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(hftw::flush_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             200 * 1024);
+        attr = true;
+    }
+    const size_t dyn = c->tma_ok ? std::min<size_t>(c->smem, 200 * 1024) : 0;
+    hftw::flush_kernel<<<c->num_sms, 512, dyn, c->stream>>>(
+        static_cast<double4*>(c->flush_buf), (long long)(bytes / 32), 1.0);
+    CUDA_TRY(c, cudaGetLastError());
     return HFTW_OK;
 }
 

@@ -381,6 +381,13 @@ __global__ void init_kernel(double* __restrict__ e, double* __restrict__ sf,
     }
 }
 
+// L2 eviction for measurements: stream-write a scratch buffer.
+__global__ void flush_kernel(double4* __restrict__ p, long long n, double v) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+         t += (long long)gridDim.x * blockDim.x)
+        p[t] = make_double4(v, v, v, v);
+}
+
 // Logical column-major dense <-> strided device layout (upload/download of
 // the KIJ store).  One thread per logical element in logical order, so the
 // dense side is coalesced.

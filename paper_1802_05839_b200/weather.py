@@ -255,6 +255,10 @@ class Context:
     def sync(self) -> None:
         self._chk(lib().hftw_sync(self._h))
 
+    def flush_l2(self, nbytes: int = 256 << 20) -> None:
+        """Measurement hook: evict the L2 on the context stream."""
+        self._chk(lib().hftw_flush_l2(self._h, nbytes))
+
     def set_stream(self, cuda_stream: int) -> None:
         self._chk(lib().hftw_set_stream(self._h, C.c_void_p(cuda_stream)))
 
