@@ -85,6 +85,8 @@ def test_b200_entry_is_measured():
     hw = m("b200")
     assert hw.bw_d and hw.bw_d > 1000
     r = P.b200_report(0.384)
-    # the paper's "with cache" model (32 B/cell) at the measured copy bandwidth
+    # the paper's "with cache" model (32 B/cell) at the measured copy bandwidth,
+    # plus the random-access boundary term ny*nz*m_ra/RA_d (perfmodel.cpp:126-154)
+    ra = (1301 * 58 * 4 / (hw.ra_d * 1e9)) if hw.ra_d else 0.0
     assert r["model_ms_per_step"]["m_sa=4"] == pytest.approx(
-        1581 * 1301 * 58 * 32 / (hw.bw_d * 1e9) * 1e3, rel=1e-3)
+        (1581 * 1301 * 58 * 32 / (hw.bw_d * 1e9) + ra) * 1e3, rel=1e-3)
