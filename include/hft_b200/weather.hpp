@@ -165,14 +165,16 @@ void reference_init(const Cfg& cfg, State& st, int device = 0) {
 }
 
 /// hft::reference_step (weather.cpp:101-171) on a host SimState, in place.
-/// Transfer-bound by construction; keep state on the device (Simulation) for
+/// Transfer-bound by construction (hftw_step_host overlaps the PCIe copies
+/// with the step in row blocks); keep state on the device (Simulation) for
 /// runs of more than one step.
 template <class Cfg, class State>
 void reference_step(const Cfg& cfg, State& st, int device = 0) {
     Simulation s(cfg, HFTW_IJK, device);
-    s.upload(st);
-    s.step(1);
-    s.download(st);
+    check(hftw_step_host(s.handle(), st.energy.data.data(), st.energy_surf.data.data(),
+                         st.energy_pbl.data.data(), st.energy.data.data(),
+                         st.energy_u.data.data()),
+          s.handle());
 }
 
 /// hft::run_reference (weather.cpp:173-178).

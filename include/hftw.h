@@ -108,6 +108,18 @@ int hftw_download(hftw_ctx* ctx, int field, double* host);
  * exactly as after the reference's buffer swap (weather.cpp:170). */
 int hftw_step(hftw_ctx* ctx, int64_t nsteps);
 
+/* hft::reference_step (weather.hpp:53-55) on a HOST SimState, end to end:
+ * energy/energy_surf/energy_pbl are the state before the step (logical
+ * column-major host arrays); energy_out and energy_u_out receive SimState's
+ * energy and energy_u after it.  energy_out may alias energy (in-place, as
+ * the reference mutates its SimState); energy_u_out must not alias the inputs.
+ * Equivalent to upload x3 + hftw_step(1) + download x2, but pipelined in
+ * row blocks so that PCIe H2D, the step kernels and PCIe D2H overlap.
+ * Synchronous; afterwards the context holds the stepped state.  Single-domain
+ * contexts only. */
+int hftw_step_host(hftw_ctx* ctx, const double* energy, const double* energy_surf,
+                   const double* energy_pbl, double* energy_out, double* energy_u_out);
+
 /* Wait for all work queued on the context stream. */
 int hftw_sync(hftw_ctx* ctx);
 

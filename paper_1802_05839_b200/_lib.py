@@ -73,6 +73,7 @@ SIGNATURES = [
     ("hftw_upload", C.c_int, [_P, C.c_int, _D]),
     ("hftw_download", C.c_int, [_P, C.c_int, _D]),
     ("hftw_step", C.c_int, [_P, C.c_int64]),
+    ("hftw_step_host", C.c_int, [_P, _D, _D, _D, _D, _D]),
     ("hftw_sync", C.c_int, [_P]),
     ("hftw_last_error", C.c_char_p, [_P]),
     ("hftw_run_reference", C.c_int, [C.POINTER(hftw_grid), C.c_int64, C.c_int, _D, _D, _D, _D]),

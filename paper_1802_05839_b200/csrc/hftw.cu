@@ -43,6 +43,7 @@ int env_int(const char* name, int dflt) {
 constexpr int kFrontPad = 31; // IJK: logical i = 1 lands on a 256-byte boundary
 constexpr int kNCW = 16;      // consumer warps of the TMA kernel
 constexpr int kChunk = 32;    // rows per TMA work unit
+constexpr int kMaxPipeBlocks = 32; // row blocks of the hftw_step_host pipeline
 
 // What a rank publishes to its neighbours (raw bytes through the caller's
 // allgather): IPC handles of the two energy buffers, sf, pb and the flags,
@@ -104,7 +105,6 @@ struct hftw_ctx {
     int* d_sched = nullptr; // work-unit counter + finished-CTA counter
     int nchunks = 0;
     int chunk = kChunk;
-    long long ghost_cells = 0;
 
     // decomposed run
     unsigned long long* flags = nullptr; // [4] step flags written by the neighbours
@@ -125,6 +125,11 @@ struct hftw_ctx {
     };
     std::vector<OutSlot> out;
     cudaStream_t copy_stream = nullptr;
+
+    // hftw_step_host: row-block pipeline H2D -> step -> D2H
+    cudaStream_t h2d_stream = nullptr, d2h_stream = nullptr;
+    std::vector<cudaEvent_t> pipe_ev;
+    double* host_stage[3] = {nullptr, nullptr, nullptr}; // dense logical energy in/out, energy_u
     void* flush_buf = nullptr;
     size_t flush_bytes = 0;
 
@@ -373,12 +378,8 @@ int setup_tma(hftw_ctx* c) {
         CUDA_TRY(c, cudaMalloc(&c->d_sched, 2 * sizeof(int)));
         CUDA_TRY(c, cudaMemset(c->d_sched, 0, 2 * sizeof(int)));
     }
-    Box o = owned_box(c);
     c->ctas = ctas;
     c->nstrips = nstrips;
-    c->ghost_cells = ((long long)(c->plan.own_s + c->plan.own_n) * nx +
-                      (long long)(c->plan.own_w + c->plan.own_e) * (o.j1 - o.j0 + 1)) *
-                     c->nz;
     c->tma_ok = true;
     return HFTW_OK;
 }
@@ -389,19 +390,59 @@ int resolved_kernel(const hftw_ctx* c) {
     return c->kernel_req;
 }
 
+// The part of one step a TMA launch covers: work units [u_lo, u_hi) of the
+// j-major order (chunk-major: unit = chunk * nstrips + strip), the i-ghost
+// columns of inner rows [gi_lo, gi_hi] and the j-ghost rows in gj_mask.
+struct StepPart {
+    int u_lo, u_hi, gi_lo, gi_hi, gj_mask;
+};
+StepPart whole_step(const hftw_ctx* c) {
+    return {0, c->nstrips * c->nchunks, 1, (int)c->lny, 3};
+}
+
+hftw::TmaArgs tma_args(const hftw_ctx* c, const StepPart& p) {
+    const hftw_plan& pl = c->plan;
+    const Box o = owned_box(c);
+    const long long gs = (p.gj_mask & 1) && pl.own_s, gn = (p.gj_mask & 2) && pl.own_n;
+    const long long r0 = std::max<long long>(p.gi_lo, 1), r1 = std::min<long long>(p.gi_hi, c->lny);
+    const long long nr = std::max<long long>(0, r1 - r0 + 1);
+    const long long ghost = ((gs + gn) * (o.i1 - o.i0 + 1) + (long long)(pl.own_w + pl.own_e) * nr) *
+                            c->nz;
+    hftw::TmaArgs a{};
+    a.fp = kFrontPad;
+    a.jrow0 = 1;
+    a.nstrips = c->nstrips;
+    a.nchunks = c->nchunks;
+    a.chunk = c->chunk;
+    a.ns = c->ns;
+    a.pk = (int)c->Pk;
+    a.ghost_cells = ghost;
+    a.sched = c->d_sched;
+    a.u_lo = p.u_lo;
+    a.u_hi = p.u_hi;
+    a.gi_lo = p.gi_lo;
+    a.gi_hi = p.gi_hi;
+    a.gj_mask = p.gj_mask;
+    return a;
+}
+
 // Launch the fused update from buf[src] into buf[src^1]; PHYS=false is the
-// diffusion-only sweep of an already post-physics field.
+// diffusion-only sweep of an already post-physics field.  `part` restricts a
+// TMA launch to a piece of the step (NULL = the whole step).
 template <bool PHYS>
-int launch_fused(hftw_ctx* c, int src, int kernel) {
+int launch_fused(hftw_ctx* c, int src, int kernel, const StepPart* part = nullptr) {
     Dom d = make_dom(c);
     Halo h = make_halo(c, src ^ 1);
     if (kernel == HFTW_KERNEL_FUSED_TMA) {
         if (!c->tma_ok) return fail(c, HFTW_EUNSUP, "TMA kernel unavailable for this grid/layout");
-        hftw::TmaArgs a{kFrontPad, 1, c->nstrips, c->nchunks, c->chunk, c->ns, (int)c->Pk,
-                        c->ghost_cells, c->d_sched};
+        const StepPart p = part ? *part : whole_step(c);
+        const hftw::TmaArgs a = tma_args(c, p);
+        // a piece with few units needs few CTAs (the ghost cells are grid-strided)
+        const long long want = std::max<long long>(p.u_hi - p.u_lo, (a.ghost_cells + 4095) / 4096);
+        const int ctas = (int)std::max<long long>(1, std::min<long long>(c->ctas, want));
         dim3 block((kNCW + 1) * 32);
 #define HFTW_LAUNCH_TMA(TX, KIJ)                                                              \
-    hftw::step_tma_kernel<TX, kNCW, PHYS, KIJ><<<c->ctas, block, c->smem, c->stream>>>(       \
+    hftw::step_tma_kernel<TX, kNCW, PHYS, KIJ><<<ctas, block, c->smem, c->stream>>>(         \
         c->tm_e[src], c->tm_sf, c->tm_pb, e3(c, src), e3(c, src ^ 1), sf2(c), pb2(c), d, a, h)
         const bool kij = c->layout == HFTW_KIJ;
         if (c->tx == 64) {
@@ -603,11 +644,19 @@ int create_common(const hftw_grid* g, int layout, int device, const hftw_plan& p
     return HFTW_OK;
 }
 
-// Host <-> device copy of the OWNED part of a 3D field.  `host` is the
-// GLOBAL logical column-major array; dev_logical points at local (0,0,1).
-int copy_3d(hftw_ctx* c, double* dev_logical, double* host, bool h2d) {
+// Host <-> device copy of the OWNED part of a 3D field (restricted to local
+// rows [r0, r1] when given).  `host` is the GLOBAL logical column-major
+// array; dev_logical points at local (0,0,1).
+int copy_3d(hftw_ctx* c, double* dev_logical, double* host, bool h2d, long long r0 = -1,
+            long long r1 = -1, cudaStream_t st = nullptr) {
+    if (!st) st = c->stream;
     const long long gnx = c->g.nx, gny = c->g.ny, nz = c->nz;
-    const Box o = owned_box(c);
+    Box o = owned_box(c);
+    if (r0 >= 0) {
+        o.j0 = std::max(o.j0, r0);
+        o.j1 = std::min(o.j1, r1);
+        if (o.j1 < o.j0) return HFTW_OK;
+    }
     const long long ni = o.i1 - o.i0 + 1, nj = o.j1 - o.j0 + 1;
     const long long gi = c->plan.gi0 + o.i0, gj = c->plan.gj0 + o.j0; // global start
     cudaPitchedPtr hp = make_cudaPitchedPtr(host, (size_t)(gnx + 2) * 8, (size_t)(gnx + 2),
@@ -632,9 +681,10 @@ int copy_3d(hftw_ctx* c, double* dev_logical, double* host, bool h2d) {
             p.dstPos = hpos;
             p.kind = cudaMemcpyDeviceToHost;
         }
-        CUDA_TRY(c, cudaMemcpy3DAsync(&p, c->stream));
+        CUDA_TRY(c, cudaMemcpy3DAsync(&p, st));
         return HFTW_OK;
     }
+    if (st != c->stream) return fail(c, HFTW_EUNSUP, "KIJ copies run on the context stream");
     // KIJ: the owned box goes through a dense device staging box
     const long long n = ni * nj * nz;
     if (c->staging_n < (size_t)n) {
@@ -669,7 +719,8 @@ int copy_3d(hftw_ctx* c, double* dev_logical, double* host, bool h2d) {
     return HFTW_OK;
 }
 
-int copy_2d(hftw_ctx* c, double* dev_logical, double* host, bool h2d) {
+int copy_2d(hftw_ctx* c, double* dev_logical, double* host, bool h2d, cudaStream_t st = nullptr) {
+    if (!st) st = c->stream;
     const long long gnx = c->g.nx;
     const Box o = owned_box(c);
     const long long ni = o.i1 - o.i0 + 1, nj = o.j1 - o.j0 + 1;
@@ -678,11 +729,9 @@ int copy_2d(hftw_ctx* c, double* dev_logical, double* host, bool h2d) {
     double* d = dev_logical + o.i0 + o.j0 * c->s2j;
     const size_t hp = (size_t)(gnx + 2) * 8, dp = (size_t)c->s2j * 8, w = (size_t)ni * 8;
     if (h2d)
-        CUDA_TRY(c, cudaMemcpy2DAsync(d, dp, h, hp, w, (size_t)nj, cudaMemcpyHostToDevice,
-                                      c->stream));
+        CUDA_TRY(c, cudaMemcpy2DAsync(d, dp, h, hp, w, (size_t)nj, cudaMemcpyHostToDevice, st));
     else
-        CUDA_TRY(c, cudaMemcpy2DAsync(h, hp, d, dp, w, (size_t)nj, cudaMemcpyDeviceToHost,
-                                      c->stream));
+        CUDA_TRY(c, cudaMemcpy2DAsync(h, hp, d, dp, w, (size_t)nj, cudaMemcpyDeviceToHost, st));
     return HFTW_OK;
 }
 
@@ -770,6 +819,11 @@ void hftw_destroy(hftw_ctx* c) {
         if (o.host) cudaFreeHost(o.host);
     }
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    if (c->h2d_stream) cudaStreamDestroy(c->h2d_stream);
+    if (c->d2h_stream) cudaStreamDestroy(c->d2h_stream);
+    for (cudaEvent_t e : c->pipe_ev) cudaEventDestroy(e);
+    for (double* p : c->host_stage)
+        if (p) cudaFree(p);
     if (c->flush_buf) cudaFree(c->flush_buf);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
@@ -1222,6 +1276,135 @@ int hftw_simulate(hftw_ctx* c, double start_time, double end_time, double timest
     if (write && (rc = deliver(true))) return rc;
     if (steps_done) *steps_done = steps;
     if (writes_done) *writes_done = writes;
+    return HFTW_OK;
+}
+
+int hftw_step_host(hftw_ctx* c, const double* energy, const double* energy_surf,
+                   const double* energy_pbl, double* energy_out, double* energy_u_out) {
+    int rc = check_ctx(c);
+    if (rc) return rc;
+    if (!energy || !energy_surf || !energy_pbl || !energy_out || !energy_u_out)
+        return fail(c, HFTW_EINVAL, "null host buffer");
+    if (c->dist)
+        return fail(c, HFTW_EUNSUP, "hftw_step_host runs on single-domain contexts");
+    double* e_in = const_cast<double*>(energy);
+    if (!c->tma_ok || c->layout != HFTW_IJK || resolved_kernel(c) != HFTW_KERNEL_FUSED_TMA) {
+        // no row-block pipeline for this configuration: the same calls in sequence
+        if ((rc = hftw_upload(c, HFTW_ENERGY, energy)) ||
+            (rc = hftw_upload(c, HFTW_ENERGY_SURF, energy_surf)) ||
+            (rc = hftw_upload(c, HFTW_ENERGY_PBL, energy_pbl)) || (rc = hftw_step(c, 1)) ||
+            (rc = hftw_download(c, HFTW_ENERGY, energy_out)) ||
+            (rc = hftw_download(c, HFTW_ENERGY_U, energy_u_out)))
+            return rc;
+        return HFTW_OK;
+    }
+    // Row blocks of whole TMA chunks.  Block b: ONE 2D H2D copy of its rows
+    // (all k) into a dense staging copy of the host array (h2d stream); on the
+    // compute stream, scatter into the padded field and -- once block b+1 has
+    // landed (the j+1 neighbours) -- the step's work units and i-ghost columns
+    // of block b's rows, energy_u of its rows and a gather of the new rows into
+    // dense staging; then ONE 2D D2H copy each of energy and energy_u (d2h
+    // stream).  The j-ghost rows need rows 1 and ny, so they run last.  H2D,
+    // the kernels and D2H overlap (PCIe is full duplex).  In-place use
+    // (energy_out == energy) is safe: a row is read back only after every row
+    // has been uploaded up to its j+1 neighbour.
+    const int nb = std::max(1, std::min(c->nchunks, std::min(kMaxPipeBlocks, env_int("HFTW_PIPE_BLOCKS", kMaxPipeBlocks))));
+    if (!c->h2d_stream) {
+        CUDA_TRY(c, cudaStreamCreateWithFlags(&c->h2d_stream, cudaStreamNonBlocking));
+        CUDA_TRY(c, cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking));
+    }
+    while ((int)c->pipe_ev.size() < 2 * kMaxPipeBlocks + 2) {
+        cudaEvent_t e;
+        CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->pipe_ev.push_back(e);
+    }
+    const long long nx = c->lnx, ny = c->lny, nz = c->nz;
+    const long long hsj = nx + 2, hsk = (nx + 2) * (ny + 2); // host (logical) strides
+    for (double*& p : c->host_stage)
+        if (!p) CUDA_TRY(c, cudaMalloc(&p, (size_t)(hsk * nz) * sizeof(double)));
+    double* const sin = c->host_stage[0];
+    double* const sout = c->host_stage[1];
+    double* const seu = c->host_stage[2];
+    cudaEvent_t* evH = c->pipe_ev.data();
+    cudaEvent_t* evC = evH + kMaxPipeBlocks;
+    cudaEvent_t evStart = evH[2 * kMaxPipeBlocks], evG = evH[2 * kMaxPipeBlocks + 1];
+    const int src = c->cur;
+    // earlier work on the context stream (steps reading buf[src]) comes first
+    CUDA_TRY(c, cudaEventRecord(evStart, c->stream));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->h2d_stream, evStart, 0));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->d2h_stream, evStart, 0));
+    if ((rc = copy_2d(c, sf2(c), const_cast<double*>(energy_surf), true, c->h2d_stream)) ||
+        (rc = copy_2d(c, pb2(c), const_cast<double*>(energy_pbl), true, c->h2d_stream)))
+        return rc;
+    auto chunk_lo = [&](int b) { return (int)((long long)b * c->nchunks / nb); };
+    auto row_lo = [&](int b) { return b == 0 ? 0LL : (long long)chunk_lo(b) * c->chunk + 1; };
+    auto row_hi = [&](int b) {
+        return b == nb - 1 ? ny + 1 : std::min<long long>(ny, (long long)chunk_lo(b + 1) * c->chunk);
+    };
+    // rows [r0, r1] of all k: nz runs of (nx+2)(r1-r0+1) doubles, one plane apart
+    const int skip = env_int("HFTW_PIPE_SKIP", 0); // tools/e2e_probe.py only: 1 = no H2D, 2 = no D2H
+    auto pcie = [&](double* dst, const double* srcp, long long r0, long long r1,
+                    cudaMemcpyKind kind, cudaStream_t st) -> int {
+        if ((skip == 1 && kind == cudaMemcpyHostToDevice) ||
+            (skip == 2 && kind == cudaMemcpyDeviceToHost))
+            return HFTW_OK;
+        const size_t pitch = (size_t)hsk * 8, width = (size_t)(hsj * (r1 - r0 + 1)) * 8;
+        CUDA_TRY(c, cudaMemcpy2DAsync(dst + r0 * hsj, pitch, srcp + r0 * hsj, pitch, width,
+                                      (size_t)nz, kind, st));
+        return HFTW_OK;
+    };
+    for (int b = 0; b < nb; ++b) {
+        if ((rc = pcie(sin, e_in, row_lo(b), row_hi(b), cudaMemcpyHostToDevice, c->h2d_stream)))
+            return rc;
+        CUDA_TRY(c, cudaEventRecord(evH[b], c->h2d_stream));
+    }
+    const Dom d = make_dom(c);
+    auto grid_rows = [&](long long r0, long long r1) {
+        return (int)std::min<long long>((r1 - r0 + 1) * nz, (long long)c->num_sms * 8);
+    };
+    auto scatter = [&](int b) -> int {
+        CUDA_TRY(c, cudaStreamWaitEvent(c->stream, evH[b], 0));
+        hftw::copy_rows_kernel<<<grid_rows(row_lo(b), row_hi(b)), 256, 0, c->stream>>>(
+            sin, hsj, hsk, e3(c, src), c->sj, c->sk, d, (int)row_lo(b), (int)row_hi(b));
+        CUDA_TRY(c, cudaGetLastError());
+        return HFTW_OK;
+    };
+    if ((rc = scatter(0))) return rc;
+    for (int b = 0; b < nb; ++b) {
+        if (b + 1 < nb && (rc = scatter(b + 1))) return rc;
+        const int ja = chunk_lo(b) * c->chunk + 1;
+        const int jb = (int)std::min<long long>(ny, (long long)chunk_lo(b + 1) * c->chunk);
+        const StepPart part{chunk_lo(b) * c->nstrips, chunk_lo(b + 1) * c->nstrips, ja, jb, 0};
+        if ((rc = launch_fused<true>(c, src, HFTW_KERNEL_FUSED_TMA, &part))) return rc;
+        const long long r0 = row_lo(b), r1 = row_hi(b);
+        hftw::physics_copy_kernel<<<grid_rows(r0, r1), 256, 0, c->stream>>>(
+            e3(c, src), seu, hsj, hsk, sf2(c), pb2(c), d, (int)r0, (int)r1);
+        hftw::copy_rows_kernel<<<grid_rows(ja, jb), 256, 0, c->stream>>>(
+            e3(c, src ^ 1), c->sj, c->sk, sout, hsj, hsk, d, ja, jb);
+        CUDA_TRY(c, cudaGetLastError());
+        CUDA_TRY(c, cudaEventRecord(evC[b], c->stream));
+        CUDA_TRY(c, cudaStreamWaitEvent(c->d2h_stream, evC[b], 0));
+        if ((rc = pcie(energy_out, sout, ja, jb, cudaMemcpyDeviceToHost, c->d2h_stream)) ||
+            (rc = pcie(energy_u_out, seu, r0, r1, cudaMemcpyDeviceToHost, c->d2h_stream)))
+            return rc;
+    }
+    const StepPart ghosts{0, 0, 1, 0, 3};
+    if ((rc = launch_fused<true>(c, src, HFTW_KERNEL_FUSED_TMA, &ghosts))) return rc;
+    for (long long r : {0LL, ny + 1})
+        hftw::copy_rows_kernel<<<grid_rows(r, r), 256, 0, c->stream>>>(
+            e3(c, src ^ 1), c->sj, c->sk, sout, hsj, hsk, d, (int)r, (int)r);
+    CUDA_TRY(c, cudaGetLastError());
+    CUDA_TRY(c, cudaEventRecord(evG, c->stream));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->d2h_stream, evG, 0));
+    if ((rc = pcie(energy_out, sout, 0, 0, cudaMemcpyDeviceToHost, c->d2h_stream)) ||
+        (rc = pcie(energy_out, sout, ny + 1, ny + 1, cudaMemcpyDeviceToHost, c->d2h_stream)))
+        return rc;
+    CUDA_TRY(c, cudaStreamSynchronize(c->d2h_stream));
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    // the context now holds the stepped state, as after upload x3 + step(1)
+    c->cur ^= 1;
+    c->eu_derived = true;
+    ++c->step_count;
     return HFTW_OK;
 }
 

@@ -344,6 +344,58 @@ __global__ void __launch_bounds__(256) physics_kij_kernel(double* __restrict__ e
     }
 }
 
+// Row-block kernels of hftw_step_host.  The host arrays use the logical
+// column-major layout (i fastest, then j, then k), so rows [j0, j1] of all k
+// are nz equal runs one host plane apart: the library stages them densely in
+// HBM in that same layout (dst/src with strides dsj, dsk) so each block
+// crosses PCIe as ONE 2D copy of nz large rows.
+//  physics_copy_kernel: dst = physics(src) (energy_u, weather.cpp:118-128).
+//  copy_rows_kernel:    dst = src (field <-> dense staging).
+// Both cover the owned columns of rows [j0, j1] (clipped to the owned rows).
+__global__ void __launch_bounds__(256) physics_copy_kernel(const double* __restrict__ src,
+                                                           double* __restrict__ dst,
+                                                           long long dsj, long long dsk,
+                                                           const double* __restrict__ sf,
+                                                           const double* __restrict__ pb,
+                                                           Dom d, int j0, int j1) {
+    Owned o = owned(d);
+    j0 = max(j0, o.j0);
+    j1 = min(j1, o.j1);
+    const int nj = j1 - j0 + 1;
+    if (nj <= 0) return;
+    const long long rows = (long long)nj * d.nz;
+    for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
+        const int j = j0 + (int)(r % nj), k = 1 + (int)(r / nj);
+        const double* s = src + j * d.sj + (long long)(k - 1) * d.sk;
+        double* t = dst + j * dsj + (long long)(k - 1) * dsk;
+        for (int i = o.i0 + threadIdx.x; i <= o.i1; i += blockDim.x) {
+            double sfv = 0.0, pbv = 0.0;
+            if (k == 1) sfv = __ldg(sf + i + j * d.s2j);
+            if (k == d.nz) pbv = __ldg(pb + i + j * d.s2j);
+            t[i] = phys<true>(__ldg(s + i * d.si), k, d.nz, sfv, pbv, d.ri, d.tv);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) copy_rows_kernel(const double* __restrict__ src,
+                                                        long long ssj, long long ssk,
+                                                        double* __restrict__ dst, long long dsj,
+                                                        long long dsk, Dom d, int j0, int j1) {
+    Owned o = owned(d);
+    j0 = max(j0, o.j0);
+    j1 = min(j1, o.j1);
+    const int nj = j1 - j0 + 1;
+    if (nj <= 0) return;
+    const long long rows = (long long)nj * d.nz;
+    for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
+        const int j = j0 + (int)(r % nj);
+        const long long k0 = r / nj;
+        const double* s = src + j * ssj + k0 * ssk;
+        double* t = dst + j * dsj + k0 * dsk;
+        for (int i = o.i0 + threadIdx.x; i <= o.i1; i += blockDim.x) t[i] = __ldg(s + i);
+    }
+}
+
 //------------------------------------------------------------------------------
 // Device-side reference_init (weather.cpp:86-98): 300 inside the integer box
 // [n/4, 3n/4] of every dimension, 0 elsewhere (buffers pre-zeroed); surface
@@ -528,6 +580,14 @@ struct TmaArgs {
     int pk;        // KIJ column pitch (doubles)
     long long ghost_cells;
     int* sched;    // [0] next work unit, [1] CTAs finished (self-resetting)
+    // Sub-range launches (hftw_step_host pipelines a step in row blocks):
+    // units [u_lo, u_hi) of the j-major order, the i-ghost columns of rows
+    // [gi_lo, gi_hi] (clipped to the owned inner rows) and the j-ghost rows
+    // in gj_mask (bit 0 = j = 0, bit 1 = j = ny+1; owned rows only).  A whole
+    // step is u = [0, units), rows [1, ny], mask 3.
+    int u_lo, u_hi;
+    int gi_lo, gi_hi;
+    int gj_mask;
 };
 
 // Post-physics value of a slab element for a cell that is NOT on k = 1 / nz.
@@ -641,7 +701,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     uint64_t* empty = full + NS;
     int* slot_unit = reinterpret_cast<int*>(empty + NS); // work unit of each staged slab
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int units = a.nstrips * a.nchunks;
+    const int units = a.u_hi - a.u_lo;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < NS; ++s) {
@@ -660,8 +720,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
         if (lane == 0) {
             uint32_t L = 0;
             for (;;) {
-                const int unit = atomicAdd(&a.sched[0], 1);
-                const bool stop = unit >= units;
+                const int unit = a.u_lo + atomicAdd(&a.sched[0], 1);
+                const bool stop = unit >= a.u_hi;
                 int ja = 0, jb = -1, ic = 0;
                 if (!stop) {
                     const int ch = unit / a.nstrips, st = unit % a.nstrips;
@@ -792,22 +852,28 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     // reference, 0.3% of the cells at ASUCA size), straight from global.
     halo_wait(h, 0xF);
     {
-        Owned o = owned(d);
-        const long long nrow = (long long)d.nx * d.nz; // one j-ghost row, i in 1..nx
-        const long long njg = (long long)(d.own_s + d.own_n) * nrow;
-        const long long ncol = (long long)(o.j1 - o.j0 + 1) * d.nz;
+        // j-ghost rows span every owned i (the corners take the i-ghost rule
+        // inside cell_update); i-ghost columns span the inner rows [r0, r1]
+        const Owned o = owned(d);
+        const int gs = (a.gj_mask & 1) && d.own_s, gn = (a.gj_mask & 2) && d.own_n;
+        const int ni = o.i1 - o.i0 + 1;
+        const long long nrow = (long long)ni * d.nz;
+        const long long njg = (long long)(gs + gn) * nrow;
+        const int r0 = max(a.gi_lo, 1), r1 = min(a.gi_hi, d.ny);
+        const int nr = max(0, r1 - r0 + 1);
+        const long long ncol = (long long)nr * d.nz;
         const long long tid = (long long)blockIdx.x * (NCW * 32) + threadIdx.x;
         for (long long g = tid; g < a.ghost_cells; g += (long long)gridDim.x * (NCW * 32)) {
             int i, j, k;
             if (g < njg) {
                 const long long which = g / nrow, rem = g % nrow;
-                i = 1 + (int)(rem % d.nx);
-                k = 1 + (int)(rem / d.nx);
-                j = (which == 0 && d.own_s) ? 0 : d.ny + 1;
+                i = o.i0 + (int)(rem % ni);
+                k = 1 + (int)(rem / ni);
+                j = (which == 0 && gs) ? 0 : d.ny + 1;
             } else {
                 const long long h = g - njg, which = h / ncol, rem = h % ncol;
-                j = o.j0 + (int)(rem % (o.j1 - o.j0 + 1));
-                k = 1 + (int)(rem / (o.j1 - o.j0 + 1));
+                j = r0 + (int)(rem % nr);
+                k = 1 + (int)(rem / nr);
                 i = (which == 0 && d.own_w) ? 0 : d.nx + 1;
             }
             const double v = cell_update<PHYS>(e, sf, pb, d, i, j, k);

@@ -246,6 +246,25 @@ class Context:
     def step(self, n: int = 1) -> None:
         self._chk(lib().hftw_step(self._h, n))
 
+    def step_host(self, energy: np.ndarray, energy_surf: np.ndarray, energy_pbl: np.ndarray,
+                  energy_out: Optional[np.ndarray] = None,
+                  energy_u_out: Optional[np.ndarray] = None) -> Tuple[np.ndarray, np.ndarray]:
+        """hftw_step_host: one reference_step on host arrays (logical column-major),
+        with H2D, the step and D2H pipelined in row blocks.  Returns
+        (energy, energy_u) after the step; energy_out may be ``energy``."""
+        n3 = (self.cfg.nx + 2) * (self.cfg.ny + 2) * self.cfg.nz
+        if energy_out is None:
+            energy_out = np.empty(n3)
+        if energy_u_out is None:
+            energy_u_out = np.empty(n3)
+        for a in (energy, energy_surf, energy_pbl, energy_out, energy_u_out):
+            if a.dtype != np.float64 or not a.flags.c_contiguous:
+                raise ValueError("host arrays must be contiguous float64")
+        self._chk(lib().hftw_step_host(self._h, _dptr(energy), _dptr(energy_surf),
+                                       _dptr(energy_pbl), _dptr(energy_out),
+                                       _dptr(energy_u_out)))
+        return energy_out, energy_u_out
+
     def physics(self, mode: int = 0) -> None:
         self._chk(lib().hftw_physics(self._h, mode))
 
@@ -361,14 +380,15 @@ def reference_init(cfg: GridConfig, st: SimState, device: int = 0) -> None:
 def reference_step(cfg: GridConfig, st: SimState, device: int = 0) -> None:
     """hft::reference_step (weather.cpp:101-171) on a host SimState, in place.
 
-    Drop-in but transfer-bound; keep the state on the device with ``Context``
-    for real runs."""
+    Drop-in but transfer-bound (hftw_step_host pipelines the PCIe copies with
+    the kernels); keep the state on the device with ``Context`` for real runs."""
     with Context(cfg, device=device) as ctx:
-        ctx.upload_state(st)
-        ctx.step(1)
-        new = ctx.download_state()
-    st.energy, st.energy_u, st.energy_surf, st.energy_pbl = (
-        new.energy, new.energy_u, new.energy_surf, new.energy_pbl)
+        e = np.ascontiguousarray(st.energy.data, dtype=np.float64)
+        eu = np.empty_like(e)
+        ctx.step_host(e, np.ascontiguousarray(st.energy_surf.data, dtype=np.float64),
+                      np.ascontiguousarray(st.energy_pbl.data, dtype=np.float64), e, eu)
+    st.energy = ArrayObject(st.energy.bounds, e)
+    st.energy_u = ArrayObject(st.energy_u.bounds, eu)
 
 
 def run_reference(cfg: GridConfig, steps: int, device: int = 0) -> SimState:
