@@ -63,7 +63,9 @@ enum hftw_kernel {
     HFTW_KERNEL_AUTO = 0,
     HFTW_KERNEL_FUSED_TMA = 1, /* fused physics+diffusion, TMA row-slab pipeline */
     HFTW_KERNEL_FUSED_CELL = 2, /* fused physics+diffusion, one cell per thread */
-    HFTW_KERNEL_SPLIT = 3       /* reference structure: physics pass, then diffusion pass */
+    HFTW_KERNEL_SPLIT = 3,      /* reference structure: physics pass, then diffusion pass */
+    HFTW_KERNEL_FUSED_PAIR = 4  /* two fused steps per pass over HBM (the intermediate field
+                                   stays on chip), single-step TMA launches for the rest */
 };
 
 enum hftw_error {
@@ -142,6 +144,13 @@ void* hftw_stream(hftw_ctx* ctx);
 int hftw_set_kernel(hftw_ctx* ctx, int kernel);
 /* Kernel actually used by hftw_step (resolves AUTO). */
 int hftw_get_kernel(const hftw_ctx* ctx);
+
+/* Measurement hook: when on, every step launch is bracketed by CUDA events on
+ * the context stream.  hftw_get_timing returns the summed device time (ms)
+ * and the number of launches of one launch kind since timing was switched
+ * on: kind 0 = single-step kernels, 1 = two-step (pair) kernels. */
+int hftw_set_timing(hftw_ctx* ctx, int on);
+int hftw_get_timing(hftw_ctx* ctx, int kind, double* ms, int64_t* launches);
 
 /* Phase 1 alone (weather.cpp:118-128): in-place column physics on ENERGY.
  * mode 0 = one column per thread with the k loop in registers (the

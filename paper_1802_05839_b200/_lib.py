@@ -16,7 +16,7 @@ HFTW_ENERGY, HFTW_ENERGY_U, HFTW_ENERGY_SURF, HFTW_ENERGY_PBL = range(4)
 FIELDS = {"energy": HFTW_ENERGY, "energy_u": HFTW_ENERGY_U,
           "energy_surf": HFTW_ENERGY_SURF, "energy_pbl": HFTW_ENERGY_PBL}
 LAYOUTS = {"ijk": 0, "kij": 1}
-KERNELS = {"auto": 0, "fused_tma": 1, "fused_cell": 2, "split": 3}
+KERNELS = {"auto": 0, "fused_tma": 1, "fused_cell": 2, "split": 3, "fused_pair": 4}
 KERNEL_NAMES = {v: k for k, v in KERNELS.items()}
 ERRORS = {0: "ok", 1: "EINVAL", 2: "ECUDA", 3: "ENOMEM", 4: "ESTATE", 5: "EUNSUP"}
 
@@ -75,6 +75,8 @@ SIGNATURES = [
     ("hftw_step", C.c_int, [_P, C.c_int64]),
     ("hftw_step_host", C.c_int, [_P, _D, _D, _D, _D, _D]),
     ("hftw_sync", C.c_int, [_P]),
+    ("hftw_set_timing", C.c_int, [_P, C.c_int]),
+    ("hftw_get_timing", C.c_int, [_P, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
     ("hftw_last_error", C.c_char_p, [_P]),
     ("hftw_run_reference", C.c_int, [C.POINTER(hftw_grid), C.c_int64, C.c_int, _D, _D, _D, _D]),
     ("hftw_set_stream", C.c_int, [_P, _P]),

@@ -26,6 +26,7 @@
 
 #include "../../include/hftw.h"
 #include "weather_kernels.cuh"
+#include "weather_pair.cuh"
 
 using hftw::Dom;
 using hftw::Halo;
@@ -49,8 +50,8 @@ constexpr int kMaxPipeBlocks = 32; // row blocks of the hftw_step_host pipeline
 // allgather): IPC handles of the two energy buffers, sf, pb and the flags,
 // plus the geometry needed to address their halo slots.
 struct PeerDesc {
-    cudaIpcMemHandle_t buf[2], sf, pb, flags;
-    long long off3, off2, si, sj, sk, s2j;
+    cudaIpcMemHandle_t buf[2], sf, flags; // sf's allocation also holds pb (n2 further)
+    long long off3, off2, si, sj, sk, s2j, n2;
     hftw_plan plan;
     int magic;
 };
@@ -105,6 +106,21 @@ struct hftw_ctx {
     int* d_sched = nullptr; // work-unit counter + finished-CTA counter
     int nchunks = 0;
     int chunk = kChunk;
+
+    // pair kernel (two steps per pass; single-domain IJK, nz <= 64)
+    bool pair_ok = false;
+    bool pair_auto = false;     // AUTO picks the pair kernel (once it beats single steps)
+    int pair_ns = 0, pair_chunk = 0, pair_nchunks = 0, pair_ctas = 0;
+    size_t pair_smem = 0;
+    CUtensorMap tm_ef[2]{};             // e: 2-wide far-column boxes
+    CUtensorMap tm_sfpb{}, tm_sfpbf{};  // [sf; pb]: slab rows / far pair
+    int* d_pair = nullptr;      // sched[2] + cnt_col[nchunks] + cnt_row[nstrips]
+    double* gcol = nullptr;     // [4][ny+2][nz]
+    double* grow = nullptr;     // [4][nz][nx+2]
+
+    // measurement hook (hftw_set_timing)
+    bool timing = false;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> tev;
 
     // decomposed run
     unsigned long long* flags = nullptr; // [4] step flags written by the neighbours
@@ -384,10 +400,134 @@ int setup_tma(hftw_ctx* c) {
     return HFTW_OK;
 }
 
+// The two-steps-per-pass kernel (weather_pair.cuh): IJK, single domain, nz
+// <= 64 (8 k values per thread), and a >= 4-deep slab ring next to the two
+// intermediate row buffers.  Leaves pair_ok = false otherwise.
+int setup_pair(hftw_ctx* c) {
+    c->pair_ok = false;
+    if (!c->tma_ok || c->layout != HFTW_IJK || c->dist || c->nz > 15 * 5) return HFTW_OK;
+    auto enc = encode_fn();
+    int smem_optin = 0;
+    CUDA_TRY(c, cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin,
+                                       c->device));
+    auto kern = c->nz <= 15 * 4 ? hftw::step_pair_kernel<4> : hftw::step_pair_kernel<5>;
+    cudaFuncAttributes fa{};
+    CUDA_TRY(c, cudaFuncGetAttributes(&fa, kern));
+    const int nz = (int)c->nz;
+    int ns = 0;
+    for (int cand = std::min(6, env_int("HFTW_PAIR_NS", 6)); cand >= 4; --cand)
+        if (hftw::pair_smem_bytes(nz, cand) + fa.sharedSizeBytes <= (size_t)smem_optin) {
+            ns = cand;
+            break;
+        }
+    if (!ns) return HFTW_OK;
+    c->pair_ns = ns;
+    c->pair_smem = hftw::pair_smem_bytes(nz, ns);
+    CUDA_TRY(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)c->pair_smem));
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, hftw::kPairThreads,
+                                                      c->pair_smem) != cudaSuccess ||
+        per_sm < 1) {
+        cudaGetLastError();
+        return HFTW_OK;
+    }
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const cuuint64_t dims3[3] = {(cuuint64_t)c->Pi, (cuuint64_t)c->Rows, (cuuint64_t)nz};
+    const cuuint64_t strides3[2] = {(cuuint64_t)c->Pi * 8, (cuuint64_t)(c->Pi * c->Rows) * 8};
+    const cuuint32_t box3[3] = {2, 1, (cuuint32_t)nz};
+    for (int b = 0; b < 2; ++b)
+        if (enc(&c->tm_ef[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->buf[b], dims3, strides3, box3,
+                estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return HFTW_OK;
+    // [sf; pb] as one 3D tensor {row pitch, rows, 2}: a slab's two boundary rows
+    // (box {TX+4, 1, 2}) and the far column's two values (box {2, 1, 2})
+    const cuuint64_t dimsb[3] = {(cuuint64_t)c->s2j, (cuuint64_t)c->Rows, 2};
+    const cuuint64_t stridesb[2] = {(cuuint64_t)c->s2j * 8, (cuuint64_t)c->n2 * 8};
+    const cuuint32_t boxb[3] = {(cuuint32_t)(hftw::kPairTX + 4), 1, 2};
+    const cuuint32_t boxbf[3] = {2, 1, 2};
+    if (enc(&c->tm_sfpb, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->sf, dimsb, stridesb, boxb, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
+        enc(&c->tm_sfpbf, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->sf, dimsb, stridesb, boxbf, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return HFTW_OK;
+    // rows per unit: as for the single-step kernel, with 4 halo slabs per unit
+    const long long ny = c->lny;
+    long long chunk = env_int("HFTW_PAIR_CHUNK", 0);
+    const long long slots = (long long)per_sm * c->num_sms;
+    if (chunk <= 0) {
+        double best = 1e30;
+        for (long long ch = std::min<long long>(64, ny); ch >= 1; --ch) {
+            const long long units = (long long)c->nstrips * ((ny + ch - 1) / ch);
+            const double waves = (double)((units + slots - 1) / slots);
+            const double cost = waves * (double)(ch + 4);
+            if (cost < best - 1e-9) {
+                best = cost;
+                chunk = ch;
+            }
+        }
+    }
+    c->pair_chunk = (int)std::min<long long>(chunk, ny);
+    c->pair_nchunks = (int)((ny + c->pair_chunk - 1) / c->pair_chunk);
+    const long long units = (long long)c->nstrips * c->pair_nchunks;
+    c->pair_ctas = (int)std::min<long long>(slots, units);
+    const size_t ints = 2 + (size_t)c->pair_nchunks + (size_t)c->nstrips;
+    CUDA_TRY(c, cudaMalloc(&c->d_pair, ints * sizeof(int)));
+    CUDA_TRY(c, cudaMemset(c->d_pair, 0, ints * sizeof(int)));
+    CUDA_TRY(c, cudaMalloc(&c->gcol, (size_t)(4 * (ny + 2) * c->nz) * sizeof(double)));
+    CUDA_TRY(c, cudaMalloc(&c->grow, (size_t)(4 * c->nz * (c->lnx + 2)) * sizeof(double)));
+    c->pair_ok = true;
+    return HFTW_OK;
+}
+
 int resolved_kernel(const hftw_ctx* c) {
     if (c->kernel_req == HFTW_KERNEL_AUTO)
-        return c->tma_ok ? HFTW_KERNEL_FUSED_TMA : HFTW_KERNEL_FUSED_CELL;
+        return c->pair_ok && c->pair_auto ? HFTW_KERNEL_FUSED_PAIR
+                          : c->tma_ok ? HFTW_KERNEL_FUSED_TMA : HFTW_KERNEL_FUSED_CELL;
     return c->kernel_req;
+}
+
+// Measurement hook: events around one launch (kind 0 = single step, 1 = pair).
+int timing_mark(hftw_ctx* c, int kind, bool begin) {
+    if (!c->timing) return HFTW_OK;
+    if (begin) {
+        cudaEvent_t a, b;
+        CUDA_TRY(c, cudaEventCreate(&a));
+        CUDA_TRY(c, cudaEventCreate(&b));
+        c->tev.push_back({kind, {a, b}});
+        CUDA_TRY(c, cudaEventRecord(a, c->stream));
+    } else {
+        CUDA_TRY(c, cudaEventRecord(c->tev.back().second.second, c->stream));
+    }
+    return HFTW_OK;
+}
+
+// Two fused steps in one launch: buf[src] -> buf[src ^ 1] = step(step(buf[src])).
+int launch_pair(hftw_ctx* c, int src) {
+    Dom d = make_dom(c);
+    hftw::PairArgs a{};
+    a.fp = kFrontPad;
+    a.jrow0 = 1;
+    a.nstrips = c->nstrips;
+    a.nchunks = c->pair_nchunks;
+    a.chunk = c->pair_chunk;
+    a.ns = c->pair_ns;
+    a.sched = c->d_pair;
+    a.cnt_col = c->d_pair + 2;
+    a.cnt_row = c->d_pair + 2 + c->pair_nchunks;
+    a.gcol = c->gcol;
+    a.grow = c->grow;
+    int rc = timing_mark(c, 1, true);
+    if (rc) return rc;
+    auto kern = c->nz <= 15 * 4 ? hftw::step_pair_kernel<4> : hftw::step_pair_kernel<5>;
+    kern<<<c->pair_ctas, hftw::kPairThreads, c->pair_smem, c->stream>>>(
+        c->tm_e[src], c->tm_sfpb, c->tm_ef[src], c->tm_sfpbf, e3(c, src), e3(c, src ^ 1), sf2(c),
+        pb2(c), d, a);
+    CUDA_TRY(c, cudaGetLastError());
+    return timing_mark(c, 1, false);
 }
 
 // The part of one step a TMA launch covers: work units [u_lo, u_hi) of the
@@ -625,9 +765,11 @@ int create_common(const hftw_grid* g, int layout, int device, const hftw_plan& p
     for (int b = 0; b < 2; ++b)
         if (cudaMalloc(&c->buf[b], c->n3 * sizeof(double)) != cudaSuccess)
             return bail(fail(c, HFTW_ENOMEM, "cudaMalloc of %zu bytes failed", c->n3 * 8));
-    if (cudaMalloc(&c->sf, c->n2 * sizeof(double)) != cudaSuccess ||
-        cudaMalloc(&c->pb, c->n2 * sizeof(double)) != cudaSuccess)
+    // sf and pb share one allocation (pb = sf + n2): the pair kernel loads both
+    // rows of a slab with one TMA box {TX+4, 1, 2}
+    if (cudaMalloc(&c->sf, 2 * c->n2 * sizeof(double)) != cudaSuccess)
         return bail(fail(c, HFTW_ENOMEM, "cudaMalloc of 2D fields failed"));
+    c->pb = c->sf + c->n2;
     if (cudaMalloc(&c->flags, 4 * sizeof(unsigned long long)) != cudaSuccess ||
         cudaMalloc(&c->done, sizeof(int)) != cudaSuccess)
         return bail(fail(c, HFTW_ENOMEM, "cudaMalloc of halo flags failed"));
@@ -640,6 +782,7 @@ int create_common(const hftw_grid* g, int layout, int device, const hftw_plan& p
         return bail(fail(c, HFTW_ECUDA, "initial memset failed"));
     int rc = setup_tma(c);
     if (rc) return bail(rc);
+    if ((rc = setup_pair(c))) return bail(rc);
     *out = c;
     return HFTW_OK;
 }
@@ -807,10 +950,16 @@ void hftw_destroy(hftw_ctx* c) {
     for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
     for (int b = 0; b < 2; ++b)
         if (c->buf[b]) cudaFree(c->buf[b]);
-    if (c->sf) cudaFree(c->sf);
-    if (c->pb) cudaFree(c->pb);
+    if (c->sf) cudaFree(c->sf); // also holds pb
     if (c->staging) cudaFree(c->staging);
     if (c->d_sched) cudaFree(c->d_sched);
+    if (c->d_pair) cudaFree(c->d_pair);
+    if (c->gcol) cudaFree(c->gcol);
+    if (c->grow) cudaFree(c->grow);
+    for (auto& t : c->tev) {
+        cudaEventDestroy(t.second.first);
+        cudaEventDestroy(t.second.second);
+    }
     if (c->flags) cudaFree(c->flags);
     if (c->done) cudaFree(c->done);
     for (auto& o : c->out) {
@@ -920,6 +1069,20 @@ int hftw_step(hftw_ctx* c, int64_t nsteps) {
             return fail(c, HFTW_EUNSUP, "the split (physics, then diffusion) kernel needs "
                                         "post-physics halos; use a fused kernel when decomposed");
     }
+    if (k == HFTW_KERNEL_FUSED_PAIR) {
+        if (!c->pair_ok) return fail(c, HFTW_EUNSUP, "pair kernel unavailable for this grid/layout");
+        // pairs, then one or two single steps: the last step is a single-step
+        // launch so that energy_u (physics of the field before it) stays
+        // derivable from the ping-pong partner
+        const int64_t pairs = nsteps >= 3 ? (nsteps - 1) / 2 : 0;
+        for (int64_t p = 0; p < pairs; ++p) {
+            if ((rc = launch_pair(c, c->cur))) return rc;
+            c->cur ^= 1;
+            c->step_count += 2;
+        }
+        nsteps -= 2 * pairs;
+    }
+    const int k1 = k == HFTW_KERNEL_FUSED_PAIR ? HFTW_KERNEL_FUSED_TMA : k;
     for (int64_t s = 0; s < nsteps; ++s) {
         if (k == HFTW_KERNEL_SPLIT) {
             // the reference's structure: physics in place, then diffusion
@@ -929,12 +1092,46 @@ int hftw_step(hftw_ctx* c, int64_t nsteps) {
                 return rc;
             c->eu_derived = false;
         } else {
-            if ((rc = launch_fused<true>(c, c->cur, k))) return rc;
+            if ((rc = timing_mark(c, 0, true))) return rc;
+            if ((rc = launch_fused<true>(c, c->cur, k1))) return rc;
+            if ((rc = timing_mark(c, 0, false))) return rc;
             c->eu_derived = true;
         }
         c->cur ^= 1;
         ++c->step_count;
     }
+    return HFTW_OK;
+}
+
+int hftw_set_timing(hftw_ctx* c, int on) {
+    int rc = check_ctx(c);
+    if (rc) return rc;
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    for (auto& t : c->tev) {
+        cudaEventDestroy(t.second.first);
+        cudaEventDestroy(t.second.second);
+    }
+    c->tev.clear();
+    c->timing = on != 0;
+    return HFTW_OK;
+}
+
+int hftw_get_timing(hftw_ctx* c, int kind, double* ms, int64_t* launches) {
+    int rc = check_ctx(c);
+    if (rc) return rc;
+    if (!ms || !launches) return fail(c, HFTW_EINVAL, "null output");
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    double tot = 0.0;
+    int64_t n = 0;
+    for (auto& t : c->tev) {
+        if (t.first != kind) continue;
+        float x = 0.f;
+        CUDA_TRY(c, cudaEventElapsedTime(&x, t.second.first, t.second.second));
+        tot += x;
+        ++n;
+    }
+    *ms = tot;
+    *launches = n;
     return HFTW_OK;
 }
 
@@ -985,8 +1182,11 @@ void* hftw_stream(hftw_ctx* c) { return c ? static_cast<void*>(c->stream) : null
 
 int hftw_set_kernel(hftw_ctx* c, int k) {
     if (!c) return fail(nullptr, HFTW_EINVAL, "null context");
-    if (k < HFTW_KERNEL_AUTO || k > HFTW_KERNEL_SPLIT)
+    if (k < HFTW_KERNEL_AUTO || k > HFTW_KERNEL_FUSED_PAIR)
         return fail(c, HFTW_EINVAL, "bad kernel %d", k);
+    if (k == HFTW_KERNEL_FUSED_PAIR && !c->pair_ok)
+        return fail(c, HFTW_EUNSUP, "pair kernel unavailable: needs the IJK layout, one domain, "
+                                    "nz <= 64 and the TMA kernel");
     if (k == HFTW_KERNEL_FUSED_TMA && !c->tma_ok)
         return fail(c, HFTW_EUNSUP, "TMA kernel unavailable: the slab ring for this nz does not fit shared memory");
     c->kernel_req = k;
@@ -1086,7 +1286,7 @@ int hftw_peer_export(hftw_ctx* c, void* out) {
     PeerDesc pd{};
     for (int b = 0; b < 2; ++b) CUDA_TRY(c, cudaIpcGetMemHandle(&pd.buf[b], c->buf[b]));
     CUDA_TRY(c, cudaIpcGetMemHandle(&pd.sf, c->sf));
-    CUDA_TRY(c, cudaIpcGetMemHandle(&pd.pb, c->pb));
+    pd.n2 = (long long)c->n2;
     CUDA_TRY(c, cudaIpcGetMemHandle(&pd.flags, c->flags));
     pd.off3 = c->off3;
     pd.off2 = c->off2;
@@ -1129,9 +1329,7 @@ int hftw_peer_connect(hftw_ctx* c, const void* all, int world) {
             CUDA_TRY(c, cudaIpcOpenMemHandle(&p, pd.sf, cudaIpcMemLazyEnablePeerAccess));
             c->ipc_opened.push_back(p);
             m.sf = static_cast<double*>(p) + pd.off2;
-            CUDA_TRY(c, cudaIpcOpenMemHandle(&p, pd.pb, cudaIpcMemLazyEnablePeerAccess));
-            c->ipc_opened.push_back(p);
-            m.pb = static_cast<double*>(p) + pd.off2;
+            m.pb = static_cast<double*>(p) + pd.n2 + pd.off2;
             CUDA_TRY(c, cudaIpcOpenMemHandle(&p, pd.flags, cudaIpcMemLazyEnablePeerAccess));
             c->ipc_opened.push_back(p);
             m.flags = static_cast<unsigned long long*>(p);
@@ -1288,7 +1486,9 @@ int hftw_step_host(hftw_ctx* c, const double* energy, const double* energy_surf,
     if (c->dist)
         return fail(c, HFTW_EUNSUP, "hftw_step_host runs on single-domain contexts");
     double* e_in = const_cast<double*>(energy);
-    if (!c->tma_ok || c->layout != HFTW_IJK || resolved_kernel(c) != HFTW_KERNEL_FUSED_TMA) {
+    const int rk = resolved_kernel(c);
+    if (!c->tma_ok || c->layout != HFTW_IJK ||
+        (rk != HFTW_KERNEL_FUSED_TMA && rk != HFTW_KERNEL_FUSED_PAIR)) {
         // no row-block pipeline for this configuration: the same calls in sequence
         if ((rc = hftw_upload(c, HFTW_ENERGY, energy)) ||
             (rc = hftw_upload(c, HFTW_ENERGY_SURF, energy_surf)) ||

@@ -221,3 +221,47 @@ def test_step_host_after_device_steps(coracle):
         e, eu = ctx.step_host(ref.energy.copy(), ref.energy_surf.copy(), ref.energy_pbl.copy())
     want = coracle.run_reference(g, 2)
     assert np.array_equal(e, want.energy) and np.array_equal(eu, want.energy_u)
+
+
+@pytest.mark.parametrize("shape", [(100, 37, 58), (64, 64, 2), (65, 3, 9), (2, 2, 2), (33, 200, 17),
+                                   (129, 2, 64), (128, 70, 58), (191, 97, 31), (1, 1, 1)])
+@pytest.mark.parametrize("steps", [3, 4, 5, 8])
+def test_pair_kernel_vs_oracle(coracle, shape, steps):
+    """Two steps per pass (intermediate field on chip): bitwise against the oracle on
+    ragged grids (edge strips with and without the far partner column, one-strip and
+    one-chunk grids, nz = 2) for odd and even step counts."""
+    nx, ny, nz = shape
+    if nx < 2 or ny < 2 or nz < 2:
+        pytest.skip("below the reference's minimum extents")
+    rng = np.random.default_rng(31 * nx + 7 * ny + nz + steps)
+    cfg = W.GridConfig(nx=nx, ny=ny, nz=nz, diffusion_velocity=float(rng.uniform(0, 1 / 6)),
+                       radiation_intensity=float(rng.uniform(-0.5, 0.5)),
+                       transfer_velocity=float(rng.uniform(0, 0.1)))
+    g = O.grid_from(cfg)
+    n3, n2 = O.shapes(g)
+    s0 = O.State(rng.uniform(150, 350, n3), rng.uniform(150, 350, n3),
+                 rng.uniform(150, 350, n2), rng.uniform(150, 350, n2))
+    want = coracle.steps(g, s0, steps).fields()
+    got = run_device(cfg, steps, "ijk", "fused_pair", s0.fields())
+    assert_same(got, want, f"{shape}/pair/{steps}")
+
+
+def test_pair_kernel_is_auto_and_hash(golden, coracle):
+    h = golden["hashes"]["1581x1301x58_s2"]
+    cfg = cfg_of(h["grid"])
+    # 256x256x64 x 10 steps: 4 pairs + 2 single steps
+    h = golden["hashes"]["256x256x64_s10"]
+    got = run_device(cfg_of(h["grid"]), h["steps"], "ijk", "fused_pair")
+    for f, v in h["fnv1a64"].items():
+        assert coracle.fnv(got[f]) == v, f
+
+
+def test_pair_kernel_asuca_vs_oracle(coracle):
+    """BASELINE's full size, 5 steps = 2 pairs + 1 single step, bitwise."""
+    cfg = W.GridConfig(nx=1581, ny=1301, nz=58)
+    want = coracle.run_reference(O.grid_from(cfg), 5)
+    with W.Context(cfg, kernel="fused_pair") as ctx:
+        ctx.init()
+        ctx.step(5)
+        for f in ("energy", "energy_u"):
+            assert np.array_equal(ctx.download(f), getattr(want, f)), f
