@@ -45,6 +45,10 @@ constexpr int kFrontPad = 31; // IJK: logical i = 1 lands on a 256-byte boundary
 constexpr int kNCW = 16;      // consumer warps of the TMA kernel
 constexpr int kChunk = 32;    // rows per TMA work unit
 constexpr int kMaxPipeBlocks = 32; // row blocks of the hftw_step_host pipeline
+#ifndef HFTW_PAIR_KPT
+#define HFTW_PAIR_KPT (64 / HFTW_PAIR_KG)
+#endif
+constexpr int kPairKPT = HFTW_PAIR_KPT; // planes per thread of the pair kernel (nz <= KG * KPT)
 
 // What a rank publishes to its neighbours (raw bytes through the caller's
 // allgather): IPC handles of the two energy buffers, sf, pb and the flags,
@@ -112,7 +116,9 @@ struct hftw_ctx {
     bool pair_auto = false;     // AUTO picks the pair kernel (once it beats single steps)
     int pair_ns = 0, pair_chunk = 0, pair_nchunks = 0, pair_ctas = 0;
     size_t pair_smem = 0;
+    CUtensorMap tm_e2[2]{};             // e: slab boxes {kPairW, 1, nz}
     CUtensorMap tm_ef[2]{};             // e: 2-wide far-column boxes
+    int pair_nstrips = 0;
     CUtensorMap tm_sfpb{}, tm_sfpbf{};  // [sf; pb]: slab rows / far pair
     int* d_pair = nullptr;      // sched[2] + cnt_col[nchunks] + cnt_row[nstrips]
     double* gcol = nullptr;     // [4][ny+2][nz]
@@ -405,17 +411,18 @@ int setup_tma(hftw_ctx* c) {
 // intermediate row buffers.  Leaves pair_ok = false otherwise.
 int setup_pair(hftw_ctx* c) {
     c->pair_ok = false;
-    if (!c->tma_ok || c->layout != HFTW_IJK || c->dist || c->nz > 15 * 5) return HFTW_OK;
+    if (!c->tma_ok || c->layout != HFTW_IJK || c->dist || c->nz > hftw::kPairKG * kPairKPT)
+        return HFTW_OK;
     auto enc = encode_fn();
     int smem_optin = 0;
     CUDA_TRY(c, cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin,
                                        c->device));
-    auto kern = c->nz <= 15 * 4 ? hftw::step_pair_kernel<4> : hftw::step_pair_kernel<5>;
+    auto kern = hftw::step_pair_kernel<kPairKPT>;
     cudaFuncAttributes fa{};
     CUDA_TRY(c, cudaFuncGetAttributes(&fa, kern));
     const int nz = (int)c->nz;
     int ns = 0;
-    for (int cand = std::min(6, env_int("HFTW_PAIR_NS", 6)); cand >= 4; --cand)
+    for (int cand = std::min(8, env_int("HFTW_PAIR_NS", 8)); cand >= 4; --cand)
         if (hftw::pair_smem_bytes(nz, cand) + fa.sharedSizeBytes <= (size_t)smem_optin) {
             ns = cand;
             break;
@@ -436,6 +443,12 @@ int setup_pair(hftw_ctx* c) {
     const cuuint64_t dims3[3] = {(cuuint64_t)c->Pi, (cuuint64_t)c->Rows, (cuuint64_t)nz};
     const cuuint64_t strides3[2] = {(cuuint64_t)c->Pi * 8, (cuuint64_t)(c->Pi * c->Rows) * 8};
     const cuuint32_t box3[3] = {2, 1, (cuuint32_t)nz};
+    const cuuint32_t box3s[3] = {(cuuint32_t)hftw::kPairW, 1, (cuuint32_t)nz};
+    for (int b = 0; b < 2; ++b)
+        if (enc(&c->tm_e2[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->buf[b], dims3, strides3, box3s,
+                estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return HFTW_OK;
     for (int b = 0; b < 2; ++b)
         if (enc(&c->tm_ef[b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->buf[b], dims3, strides3, box3,
                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -445,7 +458,7 @@ int setup_pair(hftw_ctx* c) {
     // (box {TX+4, 1, 2}) and the far column's two values (box {2, 1, 2})
     const cuuint64_t dimsb[3] = {(cuuint64_t)c->s2j, (cuuint64_t)c->Rows, 2};
     const cuuint64_t stridesb[2] = {(cuuint64_t)c->s2j * 8, (cuuint64_t)c->n2 * 8};
-    const cuuint32_t boxb[3] = {(cuuint32_t)(hftw::kPairTX + 4), 1, 2};
+    const cuuint32_t boxb[3] = {(cuuint32_t)hftw::kPairW, 1, 2};
     const cuuint32_t boxbf[3] = {2, 1, 2};
     if (enc(&c->tm_sfpb, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, c->sf, dimsb, stridesb, boxb, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -454,6 +467,7 @@ int setup_pair(hftw_ctx* c) {
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return HFTW_OK;
+    c->pair_nstrips = (int)((c->lnx + hftw::kPairTX - 1) / hftw::kPairTX);
     // rows per unit: as for the single-step kernel, with 4 halo slabs per unit
     const long long ny = c->lny;
     long long chunk = env_int("HFTW_PAIR_CHUNK", 0);
@@ -461,7 +475,7 @@ int setup_pair(hftw_ctx* c) {
     if (chunk <= 0) {
         double best = 1e30;
         for (long long ch = std::min<long long>(64, ny); ch >= 1; --ch) {
-            const long long units = (long long)c->nstrips * ((ny + ch - 1) / ch);
+            const long long units = (long long)c->pair_nstrips * ((ny + ch - 1) / ch);
             const double waves = (double)((units + slots - 1) / slots);
             const double cost = waves * (double)(ch + 4);
             if (cost < best - 1e-9) {
@@ -472,9 +486,9 @@ int setup_pair(hftw_ctx* c) {
     }
     c->pair_chunk = (int)std::min<long long>(chunk, ny);
     c->pair_nchunks = (int)((ny + c->pair_chunk - 1) / c->pair_chunk);
-    const long long units = (long long)c->nstrips * c->pair_nchunks;
+    const long long units = (long long)c->pair_nstrips * c->pair_nchunks;
     c->pair_ctas = (int)std::min<long long>(slots, units);
-    const size_t ints = 2 + (size_t)c->pair_nchunks + (size_t)c->nstrips;
+    const size_t ints = 2 + (size_t)c->pair_nchunks + (size_t)c->pair_nstrips;
     CUDA_TRY(c, cudaMalloc(&c->d_pair, ints * sizeof(int)));
     CUDA_TRY(c, cudaMemset(c->d_pair, 0, ints * sizeof(int)));
     CUDA_TRY(c, cudaMalloc(&c->gcol, (size_t)(4 * (ny + 2) * c->nz) * sizeof(double)));
@@ -511,7 +525,7 @@ int launch_pair(hftw_ctx* c, int src) {
     hftw::PairArgs a{};
     a.fp = kFrontPad;
     a.jrow0 = 1;
-    a.nstrips = c->nstrips;
+    a.nstrips = c->pair_nstrips;
     a.nchunks = c->pair_nchunks;
     a.chunk = c->pair_chunk;
     a.ns = c->pair_ns;
@@ -522,9 +536,9 @@ int launch_pair(hftw_ctx* c, int src) {
     a.grow = c->grow;
     int rc = timing_mark(c, 1, true);
     if (rc) return rc;
-    auto kern = c->nz <= 15 * 4 ? hftw::step_pair_kernel<4> : hftw::step_pair_kernel<5>;
+    auto kern = hftw::step_pair_kernel<kPairKPT>;
     kern<<<c->pair_ctas, hftw::kPairThreads, c->pair_smem, c->stream>>>(
-        c->tm_e[src], c->tm_sfpb, c->tm_ef[src], c->tm_sfpbf, e3(c, src), e3(c, src ^ 1), sf2(c),
+        c->tm_e2[src], c->tm_sfpb, c->tm_ef[src], c->tm_sfpbf, e3(c, src), e3(c, src ^ 1), sf2(c),
         pb2(c), d, a);
     CUDA_TRY(c, cudaGetLastError());
     return timing_mark(c, 1, false);

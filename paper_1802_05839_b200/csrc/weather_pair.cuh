@@ -9,20 +9,21 @@
 // (explicitly rounded IEEE ops, the reference's association order), so the
 // result is bitwise identical to two reference steps.
 //
-// Tiling (IJK store, one persistent CTA per SM, dynamic j-major work units of
-// 64-column strips x `chunk` rows, as in step_tma_kernel):
-//   * the producer warp streams, per row j, one TMA slab of e_s covering
-//     columns i0-2 .. i0+65 and all k, the sf/pb rows, and -- for the edge
-//     strips -- the 2-wide column holding the cyclic partner of the i-ghost
-//     cell (column nx for strip 0, column 1 for the last strip);
-//   * row j' of the intermediate P' = physics(e_{s+1}) is computed for columns
-//     i0-1 .. i0+64 from slabs j'-1, j', j'+1 (16 main warps own i0 .. i0+63,
-//     one halo warp the two halo columns) into a shared row buffer, and each
-//     main thread keeps its column's last three intermediate rows in
-//     registers (a j window);
-//   * row j = j'-1 of e_{s+2} is then computed from the row buffer (i and k
-//     neighbours) and the register window (j neighbours) and stored with
-//     256-byte coalesced stores.
+// Tiling (IJK store, one persistent 512-thread CTA per SM, dynamic j-major
+// work units of 62-column strips x `chunk` rows):
+//   * per row j, ONE TMA box of e_s covers columns i0-2 .. i0+63 and all k,
+//     one box the sf and pb rows, and -- for the two edge strips -- a 2-wide
+//     box holds the cyclic partner column of the i-ghost cell (column nx for
+//     strip 0, column 1 for the last strip).  Thread 0 refills the ring slot
+//     a row frees right after the row's barrier (no producer warp);
+//   * row jr of the intermediate P' = physics(e_{s+1}) is computed for the 64
+//     columns i0-1 .. i0+62 from slabs jr-1, jr, jr+1: 8 k-groups of <= 8
+//     planes x 64 columns = 16 warps, each thread walking its planes with a
+//     register window.  P' goes to a shared row buffer, and each thread keeps
+//     its column's last three intermediate rows in registers (a j window);
+//   * row j = jr-1 of e_{s+2} is then computed for the 62 columns i0 .. i0+61
+//     from the row buffer (i and k neighbours) and the register window (j
+//     neighbours) and stored straight to HBM.
 // Ghost cells of e_{s+2} need intermediates from the opposite edge of the
 // domain (the reference's cyclic rules, weather.cpp:152-168).  Units on the
 // domain rim publish their ghost-adjacent intermediates (columns 0, 1, nx,
@@ -35,13 +36,14 @@
 
 namespace hftw {
 
-constexpr int kPairTX = 64;                          // strip width (cells)
-constexpr int kPairKG = 15;                          // k-groups of the main threads
-constexpr int kPairMain = kPairTX * kPairKG;         // 960 main threads (30 warps)
-constexpr int kPairConsumers = kPairMain + 32;       // + the halo warp
-constexpr int kPairThreads = kPairConsumers + 32;    // + the producer warp
-constexpr int kPairIBW = kPairTX + 2;                // intermediate row: columns i0-1 .. i0+64
-constexpr int kPairW = kPairTX + 4;                  // slab row: columns i0-2 .. i0+65
+constexpr int kPairTX = 62;                     // output columns per strip
+constexpr int kPairIC = kPairTX + 2;            // intermediate columns i0-1 .. i0+62 (2 warps)
+constexpr int kPairW = kPairTX + 4;             // slab columns i0-2 .. i0+63
+#ifndef HFTW_PAIR_KG
+#define HFTW_PAIR_KG 8
+#endif
+constexpr int kPairKG = HFTW_PAIR_KG;           // k-groups (8: 512 threads, <= 8 planes each)
+constexpr int kPairThreads = kPairIC * kPairKG;
 
 __host__ __device__ inline int round128(int b) { return (b + 127) / 128 * 128; }
 
@@ -53,7 +55,7 @@ struct PairGeom {
     int fcol;   // far column: [k][2] doubles
     int fsp;    // far sf / pb pairs: [2][2] doubles
     int stage;
-    int ib;     // one intermediate row buffer: [k][IBW] doubles
+    int ib;     // one intermediate row buffer: [k][IC] doubles
     int tx_main, tx_far; // bytes the TMA delivers per stage (without / with the far column)
 };
 __host__ __device__ inline PairGeom pair_geom(int nz) {
@@ -63,14 +65,14 @@ __host__ __device__ inline PairGeom pair_geom(int nz) {
     g.fcol = round128(2 * nz * 8);
     g.fsp = 128;
     g.stage = g.slab + g.sfpb + g.fcol + g.fsp;
-    g.ib = round128(kPairIBW * nz * 8);
+    g.ib = round128(kPairIC * nz * 8);
     g.tx_main = kPairW * nz * 8 + 2 * kPairW * 8;
     g.tx_far = g.tx_main + 2 * nz * 8 + 4 * 8;
     return g;
 }
 __host__ __device__ inline size_t pair_smem_bytes(int nz, int ns) {
     const PairGeom g = pair_geom(nz);
-    return (size_t)ns * g.stage + 2 * (size_t)g.ib + 2 * ns * sizeof(uint64_t) + ns * sizeof(int);
+    return (size_t)ns * g.stage + 2 * (size_t)g.ib + ns * sizeof(uint64_t) + ns * sizeof(int);
 }
 
 struct PairArgs {
@@ -84,16 +86,12 @@ struct PairArgs {
     double* grow; // P' at j = 0, 1, ny, ny+1: [4][nz][nx+2]
 };
 
-// Which cyclic partner column a unit's far TMA column holds (0 = none).
+// Which cyclic partner column a unit's far TMA box holds (0 = none).
 __host__ __device__ inline int pair_far_col(int st, int nstrips, int nx) {
     const int i0 = 1 + st * kPairTX;
-    if (st == 0 && nx > i0 + kPairTX + 1) return nx;         // i-ghost 0 needs column nx
-    if (st == nstrips - 1 && st > 0 && i0 - 2 > 1) return 1; // i-ghost nx+1 needs column 1
+    if (st == 0 && nx > i0 + kPairTX + 1) return nx; // i-ghost 0 needs column nx
+    if (st == nstrips - 1 && st > 0) return 1;       // i-ghost nx+1 needs column 1
     return 0;
-}
-
-__device__ __forceinline__ void named_bar(int id, int n) {
-    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
 // Post-physics value of one pre-step element (weather.cpp:122-127).
@@ -103,96 +101,130 @@ __device__ __forceinline__ double Pfull(double ev, int k, int nz, double sfv, do
 }
 
 // One thread's view of the three slab rows of an intermediate row (at the
-// thread's slab column): e rows j'-1, j', j'+1 and their sf / pb rows.
+// thread's slab column): e rows jr-1, jr, jr+1 and their sf rows (the pb row
+// is kPairW doubles after each sf row).
 struct IRow {
     const double *em, *e0, *ep;
-    const double *Sm, *S0, *Sp; // sf rows (pb rows are kPairW doubles further)
+    const double *Sm, *S0, *Sp;
 };
 
 // Intermediate P' = physics(u') of an INNER cell column (1 <= gi <= nx,
-// 1 <= j' <= ny) for k = kl .. kl+nk-1 (KP >= nk; extra iterations recompute
-// the last k and are not stored).  FAST: the k window never touches k = 1 or
-// nz, so no physics correction and no k-plane formula can apply
-// (weather.cpp:122-127, :134-137 only).
-template <int KP, bool FAST>
-__device__ __forceinline__ void inter_inner(const IRow& r, double* out, double* ib, int kl, int nk,
+// 1 <= jr <= ny) for the planes kl .. kl+NK-1.  FIRST: kl == 1 (the k = 1
+// plane, weather.cpp:142-145, with the sf correction of :123-125), LAST: the
+// last plane is nz (:146-149, pb correction :126-127); every other plane is
+// the inner stencil (:130-137) with P = e + ri.  All branches are resolved at
+// compile time and every offset is a constant.
+template <int KP, int NK, bool FIRST, bool LAST>
+__device__ __forceinline__ void inter_inner(const IRow& r, double* out, double* ib, int kl,
                                             const Dom& d) {
     constexpr int W = kPairW;
-    const double ri = d.ri, dv = d.dv;
-    if (FAST) {
-        // nk == KP and 3 <= k-1, k+1 <= nz-1: every offset is a compile-time constant
-        const double* p0 = r.e0 + (kl - 1) * W;
-        const double* pm = r.em + (kl - 1) * W;
-        const double* pp = r.ep + (kl - 1) * W;
-        double* q = ib + (kl - 1) * kPairIBW;
-        const double c6 = d.c6;
-        double pd = dadd(p0[-W], ri), pc = dadd(p0[0], ri);
+    const double ri = d.ri, tv = d.tv, dv = d.dv, c6 = d.c6, c5 = d.c5;
+    const double* p0 = r.e0 + (kl - 1) * W;
+    const double* pm = r.em + (kl - 1) * W;
+    const double* pp = r.ep + (kl - 1) * W;
+    double* q = ib ? ib + (kl - 1) * kPairIC : nullptr;
+    auto corr = [&](double x, double bnd) { return dsub(x, dmul(tv, dsub(x, bnd))); };
+    const double* sfr = r.S0;     // sf row (pb is W further)
+    // window: pd = P(k-1), pc = P(k).  The fast shapes are used only when every
+    // group has >= 2 planes (nz >= 16), so the planes next to a group (kl-1,
+    // kh+1) are never 1 or nz unless the group itself is FIRST / LAST.
+    double pd = FIRST ? 0.0 : dadd(p0[-W], ri);
+    double pc = FIRST ? corr(dadd(p0[0], ri), sfr[0]) : dadd(p0[0], ri);
 #pragma unroll
-        for (int kk = 0; kk < KP; ++kk) {
-            const double pn = dadd(p0[(kk + 1) * W], ri);
-            double s = dadd(dadd(p0[kk * W - 1], ri), dadd(p0[kk * W + 1], ri));
-            s = dadd(s, dadd(pm[kk * W], ri));
-            s = dadd(s, dadd(pp[kk * W], ri));
-            const double u = dadd(dmul(c6, pc), dmul(dv, dadd(dadd(s, pd), pn)));
-            const double v = dadd(u, ri);
-            out[kk] = v;
-            q[kk * kPairIBW] = v;
-            pd = pc;
-            pc = pn;
+    for (int kk = 0; kk < NK; ++kk) {
+        const int o = kk * W;
+        const bool top = FIRST && kk == 0;       // plane 1
+        const bool bot = LAST && kk == NK - 1;   // plane nz
+        double pn = 0.0;
+        if (!bot) {
+            pn = dadd(p0[o + W], ri);
+            if (LAST && kk == NK - 2) pn = corr(pn, sfr[W]); // plane nz
         }
-        return;
+        double v;
+        if (top || bot) {
+            const int bo = top ? 0 : W;
+            double s = dadd(corr(dadd(p0[o - 1], ri), sfr[bo - 1]),
+                            corr(dadd(p0[o + 1], ri), sfr[bo + 1]));
+            s = dadd(s, corr(dadd(pm[o], ri), r.Sm[bo]));
+            s = dadd(s, corr(dadd(pp[o], ri), r.Sp[bo]));
+            const double u = dadd(dmul(c5, pc), dmul(dv, dadd(s, top ? pn : pd)));
+            v = corr(dadd(u, ri), sfr[bo]);
+        } else {
+            double s = dadd(dadd(p0[o - 1], ri), dadd(p0[o + 1], ri));
+            s = dadd(s, dadd(pm[o], ri));
+            s = dadd(s, dadd(pp[o], ri));
+            const double u = dadd(dmul(c6, pc), dmul(dv, dadd(dadd(s, pd), pn)));
+            v = dadd(u, ri);
+        }
+        out[kk] = v;
+        pd = pc;
+        pc = pn;
     }
-    const int nz = d.nz, kh = kl + nk - 1;
-    const double tv = d.tv;
-    const double* Bm = r.Sm + W;
+    // row-buffer stores after the loop: a store inside it would keep the
+    // compiler from hoisting the next plane's slab loads above it (possible
+    // shared-memory aliasing), serialising the planes
+    if (ib) {
+#pragma unroll
+        for (int kk = 0; kk < NK; ++kk) q[kk * kPairIC] = out[kk];
+    }
+}
+
+// Generic (any plane range, runtime nk <= KP): Pfull everywhere.  Used only
+// for grids whose k-groups match no compile-time shape (small or odd nz).
+template <int KP>
+__device__ __forceinline__ void inter_generic(const IRow& r, double* out, double* ib, int kl,
+                                              int nk, const Dom& d) {
+    constexpr int W = kPairW;
+    const int nz = d.nz;
+    const double ri = d.ri, tv = d.tv, dv = d.dv;
     const double* B0 = r.S0 + W;
-    const double* Bp = r.Sp + W;
     auto Pc = [&](int k) { return Pfull(r.e0[(k - 1) * W], k, nz, r.S0[0], B0[0], ri, tv); };
     double pd = kl > 1 ? Pc(kl - 1) : 0.0;
     double pc = Pc(kl);
 #pragma unroll
     for (int kk = 0; kk < KP; ++kk) {
-        const int k = min(kl + kk, kh);
+        if (kk >= nk) break;
+        const int k = kl + kk;
         const int o = (k - 1) * W;
         const double pn = k < nz ? Pc(k + 1) : 0.0;
         double s = dadd(Pfull(r.e0[o - 1], k, nz, r.S0[-1], B0[-1], ri, tv),
                         Pfull(r.e0[o + 1], k, nz, r.S0[1], B0[1], ri, tv));
-        s = dadd(s, Pfull(r.em[o], k, nz, r.Sm[0], Bm[0], ri, tv));
-        s = dadd(s, Pfull(r.ep[o], k, nz, r.Sp[0], Bp[0], ri, tv));
+        s = dadd(s, Pfull(r.em[o], k, nz, r.Sm[0], r.Sm[W], ri, tv));
+        s = dadd(s, Pfull(r.ep[o], k, nz, r.Sp[0], r.Sp[W], ri, tv));
         double u;
         if (k == 1) u = dadd(dmul(d.c5, pc), dmul(dv, dadd(s, pn)));
         else if (k == nz) u = dadd(dmul(d.c5, pc), dmul(dv, dadd(s, pd)));
         else u = dadd(dmul(d.c6, pc), dmul(dv, dadd(dadd(s, pd), pn)));
         const double v = Pfull(u, k, nz, r.S0[0], B0[0], ri, tv);
         out[kk] = v;
-        if (kk < nk) ib[(k - 1) * kPairIBW] = v;
+        ib[(k - 1) * kPairIC] = v;
         pd = pc;
         pc = pn;
     }
 }
 
-// Intermediate of a GHOST cell column (gi in {0, nx+1} or j' in {0, ny+1}),
+// Intermediate of a GHOST cell column (gi in {0, nx+1} or jr in {0, ny+1}),
 // in the reference's precedence (i ghosts first, weather.cpp:161-168, then j
 // ghosts, :152-159).  The cyclic partner comes from the slab, the far column
-// (fcol/fsf/fpb, element fsel) or -- for j ghosts -- global memory.
+// (fcol/fsp, element fsel) or -- for j ghosts -- global memory.
 template <int KP>
 __device__ __forceinline__ void inter_ghost(const IRow& r, double* out, double* ib, int kl, int nk,
                                             int gi, int jr, int cc, int i0, const Dom& d,
-                                            const double* __restrict__ e,
-                                            const double* __restrict__ sf,
-                                            const double* __restrict__ pb, const double* fcol,
-                                            const double* fsp, int fsel) {
+                                         const double* __restrict__ e,
+                                         const double* __restrict__ sf,
+                                         const double* __restrict__ pb, const double* fcol,
+                                         const double* fsp, int fsel) {
     constexpr int W = kPairW;
-    const int nz = d.nz, nx = d.nx, ny = d.ny, kh = kl + nk - 1;
+    const int nz = d.nz, nx = d.nx, ny = d.ny;
     const double ri = d.ri, tv = d.tv, dv = d.dv;
     const double* B0 = r.S0 + W;
-    const double* e0b = r.e0 - cc; // slab row j' at slab column 0
+    const double* e0b = r.e0 - cc; // slab row jr at slab column 0
     const double* s0b = r.S0 - cc;
     const double* b0b = B0 - cc;
     const bool ig = gi == 0 || gi == nx + 1;
     const int c1 = 1 - (i0 - 2), cn = nx - (i0 - 2); // slab columns of i = 1 and i = nx
     const bool in1 = c1 >= 0 && c1 < W, inn = cn >= 0 && cn < W;
-    const int jf = jr == 0 ? ny : 1; // j ghosts: the partner row read from global memory
+    const int jf = jr == 0 ? ny : 1; // j ghosts: the partner row, from global memory
     const double* ef = e + gi * d.si + jf * d.sj;
     double sff = 0.0, pbf = 0.0;
     if (!ig) {
@@ -201,7 +233,8 @@ __device__ __forceinline__ void inter_ghost(const IRow& r, double* out, double* 
     }
 #pragma unroll
     for (int kk = 0; kk < KP; ++kk) {
-        const int k = min(kl + kk, kh);
+        if (kk >= nk) break;
+        const int k = kl + kk;
         const int o = (k - 1) * W;
         const double pg = Pfull(r.e0[o], k, nz, r.S0[0], B0[0], ri, tv);
         double a, b;
@@ -211,56 +244,113 @@ __device__ __forceinline__ void inter_ghost(const IRow& r, double* out, double* 
             b = inn ? Pfull(e0b[o + cn], k, nz, s0b[cn], b0b[cn], ri, tv) : pf; // P(nx)
         } else {
             const double pf = Pfull(__ldg(ef + (long long)(k - 1) * d.sk), k, nz, sff, pbf, ri, tv);
-            // jr = 0: P(ny) far, P(1) = row j'+1; jr = ny+1: P(ny) = row j'-1, P(1) far
+            // jr = 0: P(ny) far, P(1) = row jr+1; jr = ny+1: P(ny) = row jr-1, P(1) far
             a = jr == 0 ? pf : Pfull(r.em[o], k, nz, r.Sm[0], r.Sm[W], ri, tv);
             b = jr == 0 ? Pfull(r.ep[o], k, nz, r.Sp[0], r.Sp[W], ri, tv) : pf;
         }
         const double u = dadd(dmul(d.c2, pg), dmul(dv, dadd(a, b)));
         const double v = Pfull(u, k, nz, r.S0[0], B0[0], ri, tv);
         out[kk] = v;
-        if (kk < nk) ib[(k - 1) * kPairIBW] = v;
+        ib[(k - 1) * kPairIC] = v;
     }
 }
 
 // Row j of e_{s+2} for one inner column: i and k neighbours from the row
 // buffer B (row j), j neighbours and the centre from the register window
 // (P0 = row j-1, P1 = row j, P2 = row j+1).  weather.cpp:130-150 on P'.
-template <int KP, bool FAST>
+// NK planes from kl; FIRST / LAST as for inter_inner (compile time).
+template <int KP, int NK, bool FIRST, bool LAST>
 __device__ __forceinline__ void final_row(const double* P0, const double* P1, const double* P2,
-                                          const double* B, double* q, long long sk, int kl, int nk,
+                                          const double* B, double* q, long long sk, int kl,
                                           const Dom& d) {
-    const double dv = d.dv;
-    if (FAST) {
-        const double* Bk = B + (kl - 1) * kPairIBW;
-        const double c6 = d.c6;
+    const double dv = d.dv, c6 = d.c6, c5 = d.c5;
+    const double* Bk = B + (kl - 1) * kPairIC;
 #pragma unroll
-        for (int kk = 0; kk < KP; ++kk) {
-            double s = dadd(Bk[kk * kPairIBW - 1], Bk[kk * kPairIBW + 1]);
-            s = dadd(s, P0[kk]);
-            s = dadd(s, P2[kk]);
-            const double km = kk > 0 ? P1[kk - 1] : Bk[-kPairIBW];
-            const double kp = kk + 1 < KP ? P1[kk + 1] : Bk[KP * kPairIBW];
-            *q = dadd(dmul(c6, P1[kk]), dmul(dv, dadd(dadd(s, km), kp)));
-            q += sk;
+    for (int kk = 0; kk < NK; ++kk) {
+        double s = dadd(Bk[kk * kPairIC - 1], Bk[kk * kPairIC + 1]);
+        s = dadd(s, P0[kk]);
+        s = dadd(s, P2[kk]);
+        double v;
+        if (FIRST && kk == 0) {
+            const double kp = kk + 1 < NK ? P1[kk + 1] : Bk[(kk + 1) * kPairIC];
+            v = dadd(dmul(c5, P1[kk]), dmul(dv, dadd(s, kp)));
+        } else if (LAST && kk == NK - 1) {
+            const double km = kk > 0 ? P1[kk - 1] : Bk[(kk - 1) * kPairIC];
+            v = dadd(dmul(c5, P1[kk]), dmul(dv, dadd(s, km)));
+        } else {
+            const double km = kk > 0 ? P1[kk - 1] : Bk[(kk - 1) * kPairIC];
+            const double kp = kk + 1 < NK ? P1[kk + 1] : Bk[(kk + 1) * kPairIC];
+            v = dadd(dmul(c6, P1[kk]), dmul(dv, dadd(dadd(s, km), kp)));
         }
-        return;
+        *q = v;
+        q += sk;
     }
-    const int nz = d.nz, kh = kl + nk - 1;
+}
+
+// One row of the fast shapes in ONE straight-line block: the final row j =
+// jr-1 (from the row buffer B of row j and the register window) and the
+// intermediate row jr (from the slabs).  The final's first partial sums
+// ((W + E) + S, weather.cpp:134-136 order) need nothing from row jr, so the
+// compiler can interleave them with the intermediate's chains; the
+// intermediate's row-buffer stores come last so no shared load has to wait
+// behind them.  The final value is stored only when `store` (the first two
+// rows of a unit have no final row; edge lanes have no output column).
+template <int KP, int NK, bool FIRST, bool LAST>
+__device__ __forceinline__ void row_fast(const IRow& r, double* P0, double* P1, double* P2,
+                                         double* ibrow, const double* B, double* q, long long sk,
+                                         int kl, bool store, const Dom& d) {
+    const double dv = d.dv, c6 = d.c6, c5 = d.c5;
+    const double* Bk = B + (kl - 1) * kPairIC;
+    double ps[NK], bm = 0.0, bp = 0.0;
+#pragma unroll
+    for (int kk = 0; kk < NK; ++kk)
+        ps[kk] = dadd(dadd(Bk[kk * kPairIC - 1], Bk[kk * kPairIC + 1]), P0[kk]);
+    if (!FIRST) bm = Bk[-kPairIC];        // P'(k = kl-1) of row j
+    if (!LAST) bp = Bk[NK * kPairIC];     // P'(k = kh+1) of row j
+    inter_inner<KP, NK, FIRST, LAST>(r, P2, nullptr, kl, d);
+#pragma unroll
+    for (int kk = 0; kk < NK; ++kk) {
+        const double s = dadd(ps[kk], P2[kk]);
+        const double km = kk > 0 ? P1[kk - 1] : bm;
+        const double kp = kk + 1 < NK ? P1[kk + 1] : bp;
+        double v;
+        if (FIRST && kk == 0) v = dadd(dmul(c5, P1[kk]), dmul(dv, dadd(s, kp)));
+        else if (LAST && kk == NK - 1) v = dadd(dmul(c5, P1[kk]), dmul(dv, dadd(s, km)));
+        else v = dadd(dmul(c6, P1[kk]), dmul(dv, dadd(dadd(s, km), kp)));
+        if (store) q[(long long)kk * sk] = v;
+    }
+    double* qi = ibrow + (kl - 1) * kPairIC;
+#pragma unroll
+    for (int kk = 0; kk < NK; ++kk) qi[kk * kPairIC] = P2[kk];
+}
+
+template <int KP>
+__device__ __forceinline__ void final_generic(const double* P0, const double* P1, const double* P2,
+                                           const double* B, double* q, long long sk, int kl,
+                                           int nk, const Dom& d) {
+    const int nz = d.nz;
+    const double dv = d.dv;
 #pragma unroll
     for (int kk = 0; kk < KP; ++kk) {
-        const int k = min(kl + kk, kh);
-        const int o = (k - 1) * kPairIBW;
+        if (kk >= nk) break;
+        const int k = kl + kk;
+        const int o = (k - 1) * kPairIC;
         double s = dadd(B[o - 1], B[o + 1]);
         s = dadd(s, P0[kk]);
         s = dadd(s, P2[kk]);
-        // (clamped reads: the k = 1 / nz cells do not use the missing neighbour)
-        const double km = kk > 0 ? P1[kk - 1] : B[max(o - kPairIBW, 0)];
-        const double kp = kk + 1 < nk ? P1[kk + 1] : B[min(o + kPairIBW, (nz - 1) * kPairIBW)];
         double v;
-        if (k == 1) v = dadd(dmul(d.c5, P1[kk]), dmul(dv, dadd(s, kp)));
-        else if (k == nz) v = dadd(dmul(d.c5, P1[kk]), dmul(dv, dadd(s, km)));
-        else v = dadd(dmul(d.c6, P1[kk]), dmul(dv, dadd(dadd(s, km), kp)));
-        if (kk < nk) q[(long long)kk * sk] = v;
+        if (k == 1) {
+            const double kp = kk + 1 < nk ? P1[kk + 1] : B[o + kPairIC];
+            v = dadd(dmul(d.c5, P1[kk]), dmul(dv, dadd(s, kp)));
+        } else if (k == nz) {
+            const double km = kk > 0 ? P1[kk - 1] : B[o - kPairIC];
+            v = dadd(dmul(d.c5, P1[kk]), dmul(dv, dadd(s, km)));
+        } else {
+            const double km = kk > 0 ? P1[kk - 1] : B[o - kPairIC];
+            const double kp = kk + 1 < nk ? P1[kk + 1] : B[o + kPairIC];
+            v = dadd(dmul(d.c6, P1[kk]), dmul(dv, dadd(dadd(s, km), kp)));
+        }
+        q[(long long)kk * sk] = v;
     }
 }
 
@@ -287,7 +377,7 @@ __device__ __forceinline__ void pair_publish(const double* v, int kl, int nk, in
 // chunk's i-ghost cells of e_{s+2} (rows ja..jb, plus 0 / ny+1 at the domain
 // ends): weather.cpp:164-167 on the intermediate field.
 __device__ __forceinline__ void pair_ghost_cols(const Dom& d, const PairArgs& a,
-                                                double* __restrict__ u, int ja, int jb, int tid) {
+                                             double* __restrict__ u, int ja, int jb, int tid) {
     const int nx = d.nx, ny = d.ny, nz = d.nz;
     const int r0 = ja == 1 ? 0 : ja, r1 = jb == ny ? ny + 1 : jb;
     const int nr = r1 - r0 + 1;
@@ -295,7 +385,7 @@ __device__ __forceinline__ void pair_ghost_cols(const Dom& d, const PairArgs& a,
     auto G = [&](int w, int j, int k) {
         return __ldcg(a.gcol + ((long long)w * (ny + 2) + j) * nz + (k - 1));
     };
-    for (long long t = tid; t < n; t += kPairConsumers) {
+    for (long long t = tid; t < n; t += kPairThreads) {
         const int k = 1 + (int)(t % nz);
         const long long q = t / nz;
         const int j = r0 + (int)(q % nr);
@@ -307,17 +397,17 @@ __device__ __forceinline__ void pair_ghost_cols(const Dom& d, const PairArgs& a,
 }
 
 // The second producer of a strip's j-ghost intermediates computes that
-// strip's j-ghost cells (i in i0..i0+63 clipped to 1..nx, j = 0 and ny+1):
+// strip's j-ghost cells (i in i0..i0+61 clipped to 1..nx, j = 0 and ny+1):
 // weather.cpp:155-158 on the intermediate field.
 __device__ __forceinline__ void pair_ghost_rows(const Dom& d, const PairArgs& a,
-                                                double* __restrict__ u, int i0, int tid) {
+                                             double* __restrict__ u, int i0, int tid) {
     const int nx = d.nx, ny = d.ny, nz = d.nz;
     const int ni = min(kPairTX, nx - i0 + 1);
     const long long n = 2LL * ni * nz;
     auto G = [&](int w, int i, int k) {
         return __ldcg(a.grow + ((long long)w * nz + (k - 1)) * (nx + 2) + i);
     };
-    for (long long t = tid; t < n; t += kPairConsumers) {
+    for (long long t = tid; t < n; t += kPairThreads) {
         const int i = i0 + (int)(t % ni);
         const long long q = t / ni;
         const int k = 1 + (int)(q % nz);
@@ -328,7 +418,62 @@ __device__ __forceinline__ void pair_ghost_rows(const Dom& d, const PairArgs& a,
     }
 }
 
-// KPT: k values per thread; nz <= 15*KPT (main threads; the halo warp has 16 groups).
+// Thread 0's TMA issue state: the unit and row of the next slab to load.
+struct PairProducer {
+    int unit;  // unit of the next load (-1: the stop sentinel has been issued)
+    int row;   // its row (ja-2 .. jb+2)
+    int jb;    // last inner row of that unit
+    int slot;  // ring slot of the next load
+};
+
+__device__ __forceinline__ void pair_issue(PairProducer& p, unsigned char* smem, const PairGeom& G,
+                                        uint64_t* full, int* slot_unit, int ns,
+                                        const CUtensorMap* tm_e, const CUtensorMap* tm_sfpb,
+                                        const CUtensorMap* tm_ef, const CUtensorMap* tm_sfpbf,
+                                        const PairArgs& a, int nx, int ny) {
+    if (p.unit < 0) return; // the sentinel is out: nothing left
+    const int slot = p.slot;
+    p.slot = slot + 1 == ns ? 0 : slot + 1;
+    if (p.row > p.jb + 2) {
+        // the current unit is fully issued: take the next one
+        p.unit = atomicAdd(&a.sched[0], 1);
+        if (p.unit >= a.nstrips * a.nchunks) {
+            slot_unit[slot] = -1;
+            mbar_arrive(&full[slot]); // no bytes: tells the consumers to finish
+            p.unit = -1;
+            return;
+        }
+        const int ch = p.unit / a.nstrips;
+        p.row = ch * a.chunk - 1; // ja - 2
+        p.jb = min(ny, ch * a.chunk + a.chunk);
+    }
+    const int st = p.unit % a.nstrips;
+    const int ic = a.fp + 1 + st * kPairTX - 2; // tensor i of i0 - 2 (even)
+    const int far = pair_far_col(st, a.nstrips, nx);
+    slot_unit[slot] = p.unit;
+    unsigned char* stg = smem + (size_t)slot * G.stage;
+    mbar_expect_tx(&full[slot], far ? G.tx_far : G.tx_main);
+    tma_load_3d(stg, tm_e, &full[slot], ic, a.jrow0 + p.row, 0);
+    tma_load_3d(stg + G.slab, tm_sfpb, &full[slot], ic, a.jrow0 + p.row, 0);
+    if (far) {
+        const int fx = (a.fp + far) & ~1; // even-aligned pair holding the far column
+        unsigned char* f = stg + G.slab + G.sfpb;
+        tma_load_3d(f, tm_ef, &full[slot], fx, a.jrow0 + p.row, 0);
+        tma_load_3d(f + G.fcol, tm_sfpbf, &full[slot], fx, a.jrow0 + p.row, 0);
+    }
+    ++p.row;
+}
+
+// Ring position of a load: slot and mbarrier phase parity.
+struct RingPos {
+    int slot;
+    uint32_t par;
+    __device__ __forceinline__ RingPos next(int ns) const {
+        return slot + 1 == ns ? RingPos{0, par ^ 1u} : RingPos{slot + 1, par};
+    }
+};
+
+// KPT: max k planes per thread (nz <= 8 * KPT).
 template <int KPT>
 __global__ void __launch_bounds__(kPairThreads, 1)
     step_pair_kernel(const __grid_constant__ CUtensorMap tm_e,
@@ -344,155 +489,122 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     double* const ib0 = reinterpret_cast<double*>(smem + (size_t)NS * G.stage);
     const int ibn = G.ib / 8;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NS * G.stage + 2 * (size_t)G.ib);
-    uint64_t* empty = full + NS;
-    int* slot_unit = reinterpret_cast<int*>(empty + NS);
+    int* slot_unit = reinterpret_cast<int*>(full + NS);
     __shared__ int s_flags;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int units = a.nstrips * a.nchunks;
+    const int tid = threadIdx.x;
     const int nx = d.nx, ny = d.ny, nz = d.nz;
 
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < NS; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kPairConsumers / 32);
-        }
+    PairProducer prod{0, 1, -2, 0}; // row > jb + 2: the first issue takes a unit
+    if (tid == 0) {
+        for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int s = 0; s < NS; ++s)
+            pair_issue(prod, smem, G, full, slot_unit, NS, &tm_e, &tm_sfpb, &tm_ef, &tm_sfpbf, a,
+                       nx, ny);
     }
     __syncthreads();
 
-    if (threadIdx.x >= kPairConsumers) {
-        // ---------------- producer warp ----------------
-        if (lane == 0) {
-            uint32_t L = 0;
-            for (;;) {
-                const int unit = atomicAdd(&a.sched[0], 1);
-                const bool stop = unit >= units;
-                int ja = 0, jb = -1, ic = 0, fx = 0, far = 0;
-                if (!stop) {
-                    const int ch = unit / a.nstrips, st = unit % a.nstrips;
-                    ja = ch * a.chunk + 1;
-                    jb = min(ny, ja + a.chunk - 1);
-                    ic = a.fp + 1 + st * kPairTX - 2; // tensor i of i0 - 2 (even)
-                    far = pair_far_col(st, a.nstrips, nx);
-                    fx = (a.fp + far) & ~1;           // even-aligned pair holding it
-                }
-                // rows ja-2 .. jb+2 (the slabs of intermediate rows ja-1 .. jb+1)
-                for (int jj = ja - 2; stop ? jj == ja - 2 : jj <= jb + 2; ++jj, ++L) {
-                    const uint32_t slot = L % NS;
-                    if (L >= (uint32_t)NS) mbar_wait(&empty[slot], ((L / NS) - 1) & 1);
-                    slot_unit[slot] = stop ? -1 : unit;
-                    if (stop) {
-                        mbar_arrive(&full[slot]);
-                        break;
-                    }
-                    unsigned char* stg = smem + (size_t)slot * G.stage;
-                    mbar_expect_tx(&full[slot], far ? G.tx_far : G.tx_main);
-                    tma_load_3d(stg, &tm_e, &full[slot], ic, a.jrow0 + jj, 0);
-                    tma_load_3d(stg + G.slab, &tm_sfpb, &full[slot], ic, a.jrow0 + jj, 0);
-                    if (far) {
-                        unsigned char* f = stg + G.slab + G.sfpb;
-                        tma_load_3d(f, &tm_ef, &full[slot], fx, a.jrow0 + jj, 0);
-                        tma_load_3d(f + G.fcol, &tm_sfpbf, &full[slot], fx, a.jrow0 + jj, 0);
-                    }
-                }
-                if (stop) break;
-            }
-            __threadfence();
-            if (atomicAdd(&a.sched[1], 1) == (int)gridDim.x - 1) {
-                a.sched[0] = 0;
-                a.sched[1] = 0;
-                __threadfence();
-            }
-        }
-        return;
-    }
-
-    // ---------------- consumers: 30 main warps + 1 halo warp ----------------
-    const int tid = threadIdx.x;
-    const bool halo = tid >= kPairMain;
-    // main: column c = tid % 64 (slab column c+2), k-group tid / 64 (of 15)
-    // halo: lanes 0-15 column i0-1 (slab 1), lanes 16-31 column i0+64 (slab 66), 16 k-groups
-    const int cc = halo ? (lane < 16 ? 1 : kPairTX + 2) : (tid % kPairTX) + 2;
-    const int g = halo ? (lane & 15) : tid / kPairTX;
-    // k-groups of KPT consecutive planes (the last non-empty one may be short)
-    const int kl = 1 + g * KPT, kh = min(nz, kl + KPT - 1);
-    const int nk = max(0, kh - kl + 1);
-    const bool fast = nk == KPT && kl >= 3 && kh <= nz - 2;
+    // thread -> (intermediate column cc = 1 .. 64 = logical i0-2+cc, k-group g)
+    const int cc = 1 + (tid % kPairIC);
+    const int g = tid / kPairIC;
+    // balanced k-groups: planes kl .. kh, nk = kh - kl + 1 <= KPT
+    const int kl = 1 + (g * nz) / kPairKG, kh = ((g + 1) * nz) / kPairKG;
+    const int nk = kh - kl + 1;
+    const bool kfirst = kl == 1, klast = kh == nz;
+    // compile-time row shapes: nk in {KPT, KPT-1} x (first, last); else generic
+    const int fl = (kfirst ? 1 : 0) + (klast ? 2 : 0);
+    int shape = nz < 2 * kPairKG || fl == 3 ? 16
+                : nk == KPT ? fl : nk == KPT - 1 ? 4 + fl : nk == KPT - 2 ? 8 + fl : 16;
 
     double PW0[KPT], PW1[KPT], PW2[KPT];
-    uint32_t L = 0;
+    RingPos R0{0, 0}; // ring position of the current unit's first slab (row ja-2)
     for (;;) {
-        mbar_wait(&full[L % NS], (L / NS) & 1);
-        const int unit = slot_unit[L % NS];
+        mbar_wait(&full[R0.slot], R0.par);
+        const int unit = slot_unit[R0.slot];
         if (unit < 0) break;
         const int ch = unit / a.nstrips, st = unit % a.nstrips;
         const int ja = ch * a.chunk + 1, jb = min(ny, ja + a.chunk - 1);
         const int i0 = 1 + st * kPairTX;
-        const int gi = i0 - 2 + cc; // logical i of my column
+        const int gi = i0 - 2 + cc; // logical i of my intermediate column
         const bool indom = gi <= nx + 1 && nk > 0;
+
         const bool owns_i = (gi >= i0 && gi <= min(i0 + kPairTX - 1, nx + 1)) ||
                             (st == 0 && gi == 0) || (st == a.nstrips - 1 && gi == nx + 1);
         const bool ig = gi == 0 || gi == nx + 1;
         const int fsel = (a.fp + pair_far_col(st, a.nstrips, nx)) & 1;
-        const int c = cc - 2;
-        const bool do_final = !halo && i0 + c <= nx && nk > 0;
+        const bool do_final = cc >= 2 && cc <= kPairTX + 1 && gi <= nx && nk > 0;
+        RingPos Ra = R0;         // slab jr-1
+        RingPos Rb = Ra.next(NS); // slab jr
+        RingPos Rc = Rb.next(NS); // slab jr+1
+        mbar_wait(&full[Rb.slot], Rb.par);
         for (int jr = ja - 1; jr <= jb + 1; ++jr) {
-            // slabs jr-1, jr, jr+1 have load indices L + (jr - ja) + {1, 2, 3}
-            const uint32_t l0 = L + (uint32_t)(jr - ja + 1), l1 = l0 + 1, l2 = l0 + 2;
-            if (jr == ja - 1) mbar_wait(&full[l1 % NS], (l1 / NS) & 1);
-            mbar_wait(&full[l2 % NS], (l2 / NS) & 1);
+            mbar_wait(&full[Rc.slot], Rc.par);
             double* ibrow = ib0 + (jr & 1) * ibn + (cc - 1);
+            const bool fin = do_final && jr >= ja + 1; // final row j = jr-1 is stored
+            const double* B = ib0 + ((jr - 1) & 1) * ibn + (cc - 1);
+            double* q = u + (long long)gi * d.si + (long long)(jr - 1) * d.sj +
+                        (long long)(kl - 1) * d.sk;
             if (indom) {
-                const unsigned char* sm_ = smem + (size_t)(l0 % NS) * G.stage;
-                const unsigned char* s0_ = smem + (size_t)(l1 % NS) * G.stage;
-                const unsigned char* sp_ = smem + (size_t)(l2 % NS) * G.stage;
+                const unsigned char* sm_ = smem + (size_t)Ra.slot * G.stage;
+                const unsigned char* s0_ = smem + (size_t)Rb.slot * G.stage;
+                const unsigned char* sp_ = smem + (size_t)Rc.slot * G.stage;
                 const IRow r{reinterpret_cast<const double*>(sm_) + cc,
                              reinterpret_cast<const double*>(s0_) + cc,
                              reinterpret_cast<const double*>(sp_) + cc,
                              reinterpret_cast<const double*>(sm_ + G.slab) + cc,
                              reinterpret_cast<const double*>(s0_ + G.slab) + cc,
                              reinterpret_cast<const double*>(sp_ + G.slab) + cc};
-                const bool owns_j = (jr >= ja && jr <= jb) || jr == 0 || jr == ny + 1;
-                if (ig || jr == 0 || jr == ny + 1) {
-                    const double* fb = reinterpret_cast<const double*>(s0_ + G.slab + G.sfpb);
-                    const double* fsp = reinterpret_cast<const double*>(s0_ + G.slab + G.sfpb + G.fcol);
-                    inter_ghost<KPT>(r, PW2, ibrow, kl, nk, gi, jr, cc, i0, d, e, sf, pb, fb, fsp,
-                                     fsel);
-                } else if (fast) {
-                    inter_inner<KPT, true>(r, PW2, ibrow, kl, nk, d);
-                } else {
-                    inter_inner<KPT, false>(r, PW2, ibrow, kl, nk, d);
+                const bool ghost = ig || jr == 0 || jr == ny + 1;
+                int sh = ghost ? 16 : shape;
+#if defined(HFTW_EXP_SKIP_A) // tools/ timing experiment only
+                if (jr > 0) sh = 99;
+#endif
+                switch (sh) {
+                case 0: row_fast<KPT, KPT, false, false>(r, PW0, PW1, PW2, ibrow, B, q, d.sk, kl, fin, d); break;
+                case 1: row_fast<KPT, KPT, true, false>(r, PW0, PW1, PW2, ibrow, B, q, d.sk, kl, fin, d); break;
+                case 2: row_fast<KPT, KPT, false, true>(r, PW0, PW1, PW2, ibrow, B, q, d.sk, kl, fin, d); break;
+                case 4: row_fast<KPT, KPT - 1, false, false>(r, PW0, PW1, PW2, ibrow, B, q, d.sk, kl, fin, d); break;
+                case 5: row_fast<KPT, KPT - 1, true, false>(r, PW0, PW1, PW2, ibrow, B, q, d.sk, kl, fin, d); break;
+                case 6: row_fast<KPT, KPT - 1, false, true>(r, PW0, PW1, PW2, ibrow, B, q, d.sk, kl, fin, d); break;
+                case 8: row_fast<KPT, KPT - 2, false, false>(r, PW0, PW1, PW2, ibrow, B, q, d.sk, kl, fin, d); break;
+                case 9: row_fast<KPT, KPT - 2, true, false>(r, PW0, PW1, PW2, ibrow, B, q, d.sk, kl, fin, d); break;
+                case 10: row_fast<KPT, KPT - 2, false, true>(r, PW0, PW1, PW2, ibrow, B, q, d.sk, kl, fin, d); break;
+                case 99: break;
+                default:
+                    if (ghost) {
+                        const double* fb = reinterpret_cast<const double*>(s0_ + G.slab + G.sfpb);
+                        const double* fsp =
+                            reinterpret_cast<const double*>(s0_ + G.slab + G.sfpb + G.fcol);
+                        inter_ghost<KPT>(r, PW2, ibrow, kl, nk, gi, jr, cc, i0, d, e, sf, pb, fb,
+                                         fsp, fsel);
+                    } else {
+                        inter_generic<KPT>(r, PW2, ibrow, kl, nk, d);
+                    }
+                    if (fin) final_generic<KPT>(PW0, PW1, PW2, B, q, d.sk, kl, nk, d);
+                    break;
                 }
+                const bool owns_j = (jr >= ja && jr <= jb) || jr == 0 || jr == ny + 1;
                 if (owns_i && owns_j) pair_publish<KPT>(PW2, kl, nk, gi, jr, d, a);
-            }
-            // slab jr-1 is no longer needed
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[l0 % NS]);
-            if (do_final && jr >= ja + 1) {
-                const int j = jr - 1;
-                const double* B = ib0 + (j & 1) * ibn + (cc - 1);
-                double* q = u + (long long)(i0 + c) * d.si + (long long)j * d.sj +
-                            (long long)(kl - 1) * d.sk;
-                if (fast) final_row<KPT, true>(PW0, PW1, PW2, B, q, d.sk, kl, nk, d);
-                else final_row<KPT, false>(PW0, PW1, PW2, B, q, d.sk, kl, nk, d);
             }
 #pragma unroll
             for (int kk = 0; kk < KPT; ++kk) {
                 PW0[kk] = PW1[kk];
                 PW1[kk] = PW2[kk];
             }
-            named_bar(1, kPairConsumers);
-        }
-        // the unit's last two slabs (rows jb+1, jb+2)
-        {
-            const uint32_t lend = L + (uint32_t)(jb - ja + 3);
-            __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(&empty[lend % NS]);
-                mbar_arrive(&empty[(lend + 1) % NS]);
+            __syncthreads();
+            // slab jr-1 is free: refill its slot (and, after the last row, the
+            // slots of slabs jb+1 and jb+2)
+            if (tid == 0) {
+                const int nfree = jr == jb + 1 ? 3 : 1;
+                for (int f = 0; f < nfree; ++f)
+                    pair_issue(prod, smem, G, full, slot_unit, NS, &tm_e, &tm_sfpb, &tm_ef,
+                               &tm_sfpbf, a, nx, ny);
             }
-            L = lend + 2;
+            Ra = Rb;
+            Rb = Rc;
+            Rc = Rc.next(NS);
         }
+        R0 = Rc; // slabs jb+1, jb+2 were Ra, Rb: the next unit starts after them
         // rim units: count the ghost producers; the second one computes the ghosts
         const int inc_c = (st == 0) + (st == a.nstrips - 1);
         const int inc_r = (ch == 0) + (ch == a.nchunks - 1);
@@ -511,11 +623,20 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 __threadfence();
                 s_flags = f;
             }
-            named_bar(1, kPairConsumers);
+            __syncthreads();
             const int f = s_flags;
             if (f & 1) pair_ghost_cols(d, a, u, ja, jb, tid);
             if (f & 2) pair_ghost_rows(d, a, u, i0, tid);
-            named_bar(1, kPairConsumers); // s_flags is reused by the next rim unit
+            __syncthreads(); // s_flags is reused by the next rim unit
+        }
+    }
+    // the last CTA to finish re-arms the scheduler for the next launch
+    if (tid == 0) {
+        __threadfence();
+        if (atomicAdd(&a.sched[1], 1) == (int)gridDim.x - 1) {
+            a.sched[0] = 0;
+            a.sched[1] = 0;
+            __threadfence();
         }
     }
 }
