@@ -44,6 +44,7 @@ constexpr int kPairW = kPairTX + 4;             // slab columns i0-2 .. i0+63
 #endif
 constexpr int kPairKG = HFTW_PAIR_KG;           // k-groups (8: 512 threads, <= 8 planes each)
 constexpr int kPairThreads = kPairIC * kPairKG;
+constexpr int kPairNIB = 3;                     // intermediate row buffers (rows j-1, j, j+1)
 
 __host__ __device__ inline int round128(int b) { return (b + 127) / 128 * 128; }
 
@@ -72,7 +73,7 @@ __host__ __device__ inline PairGeom pair_geom(int nz) {
 }
 __host__ __device__ inline size_t pair_smem_bytes(int nz, int ns) {
     const PairGeom g = pair_geom(nz);
-    return (size_t)ns * g.stage + 2 * (size_t)g.ib + ns * sizeof(uint64_t) + ns * sizeof(int);
+    return (size_t)ns * g.stage + kPairNIB * (size_t)g.ib + ns * sizeof(uint64_t) + ns * sizeof(int);
 }
 
 struct PairArgs {
@@ -324,6 +325,60 @@ __device__ __forceinline__ void row_fast(const IRow& r, double* P0, double* P1, 
     for (int kk = 0; kk < NK; ++kk) qi[kk * kPairIC] = P2[kk];
 }
 
+// Row j of e_{s+2} from the three intermediate row buffers (Bm = row j-1,
+// B0 = row j, Bp = row j+1) at the thread's column: weather.cpp:130-150 on P'.
+template <int NK, bool FIRST, bool LAST>
+__device__ __forceinline__ void final_smem(const double* Bm, const double* B0, const double* Bp,
+                                           double* q, long long sk, int kl, bool store,
+                                           const Dom& d) {
+    const double dv = d.dv, c6 = d.c6, c5 = d.c5;
+    const int o0 = (kl - 1) * kPairIC;
+    Bm += o0;
+    B0 += o0;
+    Bp += o0;
+    double v[NK];
+#pragma unroll
+    for (int kk = 0; kk < NK; ++kk) {
+        const int o = kk * kPairIC;
+        double s = dadd(B0[o - 1], B0[o + 1]);
+        s = dadd(s, Bm[o]);
+        s = dadd(s, Bp[o]);
+        const double pc = B0[o];
+        if (FIRST && kk == 0) v[kk] = dadd(dmul(c5, pc), dmul(dv, dadd(s, B0[o + kPairIC])));
+        else if (LAST && kk == NK - 1)
+            v[kk] = dadd(dmul(c5, pc), dmul(dv, dadd(s, B0[o - kPairIC])));
+        else
+            v[kk] = dadd(dmul(c6, pc),
+                         dmul(dv, dadd(dadd(s, B0[o - kPairIC]), B0[o + kPairIC])));
+    }
+    if (store) {
+#pragma unroll
+        for (int kk = 0; kk < NK; ++kk) q[(long long)kk * sk] = v[kk];
+    }
+}
+
+template <int KP>
+__device__ __forceinline__ void final_smem_generic(const double* Bm, const double* B0,
+                                                   const double* Bp, double* q, long long sk,
+                                                   int kl, int nk, const Dom& d) {
+    const int nz = d.nz;
+    const double dv = d.dv;
+#pragma unroll
+    for (int kk = 0; kk < KP; ++kk) {
+        if (kk >= nk) break;
+        const int k = kl + kk;
+        const int o = (k - 1) * kPairIC;
+        double s = dadd(B0[o - 1], B0[o + 1]);
+        s = dadd(s, Bm[o]);
+        s = dadd(s, Bp[o]);
+        double v;
+        if (k == 1) v = dadd(dmul(d.c5, B0[o]), dmul(dv, dadd(s, B0[o + kPairIC])));
+        else if (k == nz) v = dadd(dmul(d.c5, B0[o]), dmul(dv, dadd(s, B0[o - kPairIC])));
+        else v = dadd(dmul(d.c6, B0[o]), dmul(dv, dadd(dadd(s, B0[o - kPairIC]), B0[o + kPairIC])));
+        q[(long long)kk * sk] = v;
+    }
+}
+
 template <int KP>
 __device__ __forceinline__ void final_generic(const double* P0, const double* P1, const double* P2,
                                            const double* B, double* q, long long sk, int kl,
@@ -488,7 +543,8 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     // intermediate row buffer of row j: ib0 + (j & 1) * ibn
     double* const ib0 = reinterpret_cast<double*>(smem + (size_t)NS * G.stage);
     const int ibn = G.ib / 8;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NS * G.stage + 2 * (size_t)G.ib);
+    uint64_t* full =
+        reinterpret_cast<uint64_t*>(smem + (size_t)NS * G.stage + kPairNIB * (size_t)G.ib);
     int* slot_unit = reinterpret_cast<int*>(full + NS);
     __shared__ int s_flags;
     const int tid = threadIdx.x;
@@ -516,8 +572,9 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     int shape = nz < 2 * kPairKG || fl == 3 ? 16
                 : nk == KPT ? fl : nk == KPT - 1 ? 4 + fl : nk == KPT - 2 ? 8 + fl : 16;
 
-    double PW0[KPT], PW1[KPT], PW2[KPT];
+    double PW2[KPT]; // this row's intermediate values (for publication)
     RingPos R0{0, 0}; // ring position of the current unit's first slab (row ja-2)
+    int ibi = 0;      // row buffer of the next intermediate row (rotates over 3)
     for (;;) {
         mbar_wait(&full[R0.slot], R0.par);
         const int unit = slot_unit[R0.slot];
@@ -527,23 +584,20 @@ __global__ void __launch_bounds__(kPairThreads, 1)
         const int i0 = 1 + st * kPairTX;
         const int gi = i0 - 2 + cc; // logical i of my intermediate column
         const bool indom = gi <= nx + 1 && nk > 0;
-
         const bool owns_i = (gi >= i0 && gi <= min(i0 + kPairTX - 1, nx + 1)) ||
                             (st == 0 && gi == 0) || (st == a.nstrips - 1 && gi == nx + 1);
         const bool ig = gi == 0 || gi == nx + 1;
         const int fsel = (a.fp + pair_far_col(st, a.nstrips, nx)) & 1;
         const bool do_final = cc >= 2 && cc <= kPairTX + 1 && gi <= nx && nk > 0;
-        RingPos Ra = R0;         // slab jr-1
+        RingPos Ra = R0;          // slab jr-1
         RingPos Rb = Ra.next(NS); // slab jr
         RingPos Rc = Rb.next(NS); // slab jr+1
         mbar_wait(&full[Rb.slot], Rb.par);
         for (int jr = ja - 1; jr <= jb + 1; ++jr) {
             mbar_wait(&full[Rc.slot], Rc.par);
-            double* ibrow = ib0 + (jr & 1) * ibn + (cc - 1);
-            const bool fin = do_final && jr >= ja + 1; // final row j = jr-1 is stored
-            const double* B = ib0 + ((jr - 1) & 1) * ibn + (cc - 1);
-            double* q = u + (long long)gi * d.si + (long long)(jr - 1) * d.sj +
-                        (long long)(kl - 1) * d.sk;
+            // row buffers: jr -> ibi, jr-1 -> ibi-1, jr-2 -> ibi-2 (mod 3)
+            const int ib1 = ibi == 0 ? 2 : ibi - 1, ib2 = ib1 == 0 ? 2 : ib1 - 1;
+            double* ibrow = ib0 + ibi * ibn + (cc - 1);
             if (indom) {
                 const unsigned char* sm_ = smem + (size_t)Ra.slot * G.stage;
                 const unsigned char* s0_ = smem + (size_t)Rb.slot * G.stage;
@@ -555,21 +609,13 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                              reinterpret_cast<const double*>(s0_ + G.slab) + cc,
                              reinterpret_cast<const double*>(sp_ + G.slab) + cc};
                 const bool ghost = ig || jr == 0 || jr == ny + 1;
-                int sh = ghost ? 16 : shape;
-#if defined(HFTW_EXP_SKIP_A) // tools/ timing experiment only
-                if (jr > 0) sh = 99;
-#endif
-                switch (sh) {
-                case 0: row_fast<KPT, KPT, false, false>(r, PW0, PW1, PW2, ibrow, B, q, d.sk, kl, fin, d); break;
-                case 1: row_fast<KPT, KPT, true, false>(r, PW0, PW1, PW2, ibrow, B, q, d.sk, kl, fin, d); break;
-                case 2: row_fast<KPT, KPT, false, true>(r, PW0, PW1, PW2, ibrow, B, q, d.sk, kl, fin, d); break;
-                case 4: row_fast<KPT, KPT - 1, false, false>(r, PW0, PW1, PW2, ibrow, B, q, d.sk, kl, fin, d); break;
-                case 5: row_fast<KPT, KPT - 1, true, false>(r, PW0, PW1, PW2, ibrow, B, q, d.sk, kl, fin, d); break;
-                case 6: row_fast<KPT, KPT - 1, false, true>(r, PW0, PW1, PW2, ibrow, B, q, d.sk, kl, fin, d); break;
-                case 8: row_fast<KPT, KPT - 2, false, false>(r, PW0, PW1, PW2, ibrow, B, q, d.sk, kl, fin, d); break;
-                case 9: row_fast<KPT, KPT - 2, true, false>(r, PW0, PW1, PW2, ibrow, B, q, d.sk, kl, fin, d); break;
-                case 10: row_fast<KPT, KPT - 2, false, true>(r, PW0, PW1, PW2, ibrow, B, q, d.sk, kl, fin, d); break;
-                case 99: break;
+                switch (ghost ? 16 : shape) {
+                case 0: inter_inner<KPT, KPT, false, false>(r, PW2, ibrow, kl, d); break;
+                case 1: inter_inner<KPT, KPT, true, false>(r, PW2, ibrow, kl, d); break;
+                case 2: inter_inner<KPT, KPT, false, true>(r, PW2, ibrow, kl, d); break;
+                case 4: inter_inner<KPT, KPT - 1, false, false>(r, PW2, ibrow, kl, d); break;
+                case 5: inter_inner<KPT, KPT - 1, true, false>(r, PW2, ibrow, kl, d); break;
+                case 6: inter_inner<KPT, KPT - 1, false, true>(r, PW2, ibrow, kl, d); break;
                 default:
                     if (ghost) {
                         const double* fb = reinterpret_cast<const double*>(s0_ + G.slab + G.sfpb);
@@ -580,26 +626,38 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                     } else {
                         inter_generic<KPT>(r, PW2, ibrow, kl, nk, d);
                     }
-                    if (fin) final_generic<KPT>(PW0, PW1, PW2, B, q, d.sk, kl, nk, d);
                     break;
                 }
                 const bool owns_j = (jr >= ja && jr <= jb) || jr == 0 || jr == ny + 1;
                 if (owns_i && owns_j) pair_publish<KPT>(PW2, kl, nk, gi, jr, d, a);
             }
-#pragma unroll
-            for (int kk = 0; kk < KPT; ++kk) {
-                PW0[kk] = PW1[kk];
-                PW1[kk] = PW2[kk];
-            }
-            __syncthreads();
-            // slab jr-1 is free: refill its slot (and, after the last row, the
-            // slots of slabs jb+1 and jb+2)
+            __syncthreads(); // intermediate row jr complete; slab jr-1 free
+            // refill slab jr-1's slot (and, after the last row, those of jb+1, jb+2)
             if (tid == 0) {
                 const int nfree = jr == jb + 1 ? 3 : 1;
                 for (int f = 0; f < nfree; ++f)
                     pair_issue(prod, smem, G, full, slot_unit, NS, &tm_e, &tm_sfpb, &tm_ef,
                                &tm_sfpbf, a, nx, ny);
             }
+            if (do_final && jr >= ja + 1) {
+                // row j = jr-1 of e_{s+2} from intermediate rows jr-2, jr-1, jr
+                const double* Bm = ib0 + ib2 * ibn + (cc - 1);
+                const double* B0 = ib0 + ib1 * ibn + (cc - 1);
+                const double* Bp = ib0 + ibi * ibn + (cc - 1);
+                double* q = u + (long long)gi * d.si + (long long)(jr - 1) * d.sj +
+                            (long long)(kl - 1) * d.sk;
+                switch (shape) {
+                case 0: final_smem<KPT, false, false>(Bm, B0, Bp, q, d.sk, kl, true, d); break;
+                case 1: final_smem<KPT, true, false>(Bm, B0, Bp, q, d.sk, kl, true, d); break;
+                case 2: final_smem<KPT, false, true>(Bm, B0, Bp, q, d.sk, kl, true, d); break;
+                case 4: final_smem<KPT - 1, false, false>(Bm, B0, Bp, q, d.sk, kl, true, d); break;
+                case 5: final_smem<KPT - 1, true, false>(Bm, B0, Bp, q, d.sk, kl, true, d); break;
+                case 6: final_smem<KPT - 1, false, true>(Bm, B0, Bp, q, d.sk, kl, true, d); break;
+                default: final_smem_generic<KPT>(Bm, B0, Bp, q, d.sk, kl, nk, d); break;
+                }
+            }
+            __syncthreads(); // the final row is done reading buffer ib2 (next row's target)
+            ibi = ibi == 2 ? 0 : ibi + 1;
             Ra = Rb;
             Rb = Rc;
             Rc = Rc.next(NS);

@@ -265,6 +265,17 @@ class Context:
                                        _dptr(energy_u_out)))
         return energy_out, energy_u_out
 
+    def set_timing(self, on: bool) -> None:
+        """Measurement hook: CUDA events around every step launch (hftw_set_timing)."""
+        self._chk(lib().hftw_set_timing(self._h, 1 if on else 0))
+
+    def timing(self, kind: int) -> Tuple[float, int]:
+        """(summed device ms, launches) of one launch kind since set_timing(True):
+        0 = single-step kernels, 1 = two-step (pair) kernels."""
+        ms, n = C.c_double(), C.c_int64()
+        self._chk(lib().hftw_get_timing(self._h, kind, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
+
     def physics(self, mode: int = 0) -> None:
         self._chk(lib().hftw_physics(self._h, mode))
 
