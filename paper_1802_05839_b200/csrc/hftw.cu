@@ -27,6 +27,7 @@
 #include "../../include/hftw.h"
 #include "weather_kernels.cuh"
 #include "weather_pair.cuh"
+#include "weather_wave.cuh"
 
 using hftw::Dom;
 using hftw::Halo;
@@ -123,6 +124,11 @@ struct hftw_ctx {
     int* d_pair = nullptr;      // sched[2] + cnt_col[nchunks] + cnt_row[nstrips]
     double* gcol = nullptr;     // [4][ny+2][nz]
     double* grow = nullptr;     // [4][nz][nx+2]
+
+    // multi-step wavefront launch (weather_wave.cuh): single-domain IJK
+    bool wave_ok = false;
+    int wave_chunk = 0, wave_nchunks = 0, wave_ctas = 0, wave_gtasks = 0;
+    int* d_wave = nullptr;      // sched[2] + chunk_done[nchunks] + ghost_done[1]
 
     // measurement hook (hftw_set_timing)
     bool timing = false;
@@ -546,6 +552,64 @@ int launch_pair(hftw_ctx* c, int src) {
     return timing_mark(c, 1, false);
 }
 
+// K steps per launch with the TMA kernel's tiling (weather_wave.cuh): single
+// domain, IJK, same slab ring as the single-step kernel.
+int setup_wave(hftw_ctx* c) {
+    c->wave_ok = false;
+    if (!c->tma_ok || c->layout != HFTW_IJK || c->dist || c->tx != 64 || env_int("HFTW_NO_WAVE", 0))
+        return HFTW_OK;
+    auto kern = hftw::step_wave_kernel<64, kNCW>;
+    CUDA_TRY(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)c->smem));
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (kNCW + 1) * 32, c->smem) !=
+            cudaSuccess ||
+        per_sm < 1) {
+        cudaGetLastError();
+        return HFTW_OK;
+    }
+    // Long units: the launch's tail is paid once per call, not once per step,
+    // and fewer chunk boundaries mean fewer halo rows re-read from HBM.
+    const long long ny = c->lny;
+    const long long chunk = std::min<long long>(ny, env_int("HFTW_WAVE_CHUNK", 32));
+    c->wave_chunk = (int)chunk;
+    c->wave_nchunks = (int)((ny + chunk - 1) / chunk);
+    c->wave_gtasks = std::max(1, std::min(16, (int)((c->lnx + 2) * c->nz / 2048)));
+    const long long units = (long long)c->nstrips * c->wave_nchunks + c->wave_gtasks;
+    c->wave_ctas = (int)std::min<long long>((long long)per_sm * c->num_sms, units);
+    const size_t ints = 2 + (size_t)c->wave_nchunks + 1;
+    CUDA_TRY(c, cudaMalloc(&c->d_wave, ints * sizeof(int)));
+    CUDA_TRY(c, cudaMemset(c->d_wave, 0, ints * sizeof(int)));
+    c->wave_ok = true;
+    return HFTW_OK;
+}
+
+// nsteps single steps in ONE launch (buf[src] holds the field of step 0).
+int launch_wave(hftw_ctx* c, int src, int64_t nsteps) {
+    Dom d = make_dom(c);
+    hftw::WaveArgs a{};
+    a.fp = kFrontPad;
+    a.jrow0 = 1;
+    a.nstrips = c->nstrips;
+    a.nchunks = c->wave_nchunks;
+    a.chunk = c->wave_chunk;
+    a.ns = c->ns;
+    a.nsteps = (int)nsteps;
+    a.gtasks = c->wave_gtasks;
+    a.sched = c->d_wave;
+    a.chunk_done = c->d_wave + 2;
+    a.ghost_done = c->d_wave + 2 + c->wave_nchunks;
+    a.buf0 = e3(c, src);
+    a.buf1 = e3(c, src ^ 1);
+    int rc = timing_mark(c, 2, true);
+    if (rc) return rc;
+    hftw::step_wave_kernel<64, kNCW><<<c->wave_ctas, (kNCW + 1) * 32, c->smem, c->stream>>>(
+        c->tm_e[src], c->tm_e[src ^ 1], c->tm_sf, c->tm_pb, sf2(c), pb2(c), d, a);
+    CUDA_TRY(c, cudaGetLastError());
+    return timing_mark(c, 2, false);
+}
+
+
 // The part of one step a TMA launch covers: work units [u_lo, u_hi) of the
 // j-major order (chunk-major: unit = chunk * nstrips + strip), the i-ghost
 // columns of inner rows [gi_lo, gi_hi] and the j-ghost rows in gj_mask.
@@ -799,6 +863,7 @@ int create_common(const hftw_grid* g, int layout, int device, const hftw_plan& p
     int rc = setup_tma(c);
     if (rc) return bail(rc);
     if ((rc = setup_pair(c))) return bail(rc);
+    if ((rc = setup_wave(c))) return bail(rc);
     *out = c;
     return HFTW_OK;
 }
@@ -970,6 +1035,7 @@ void hftw_destroy(hftw_ctx* c) {
     if (c->staging) cudaFree(c->staging);
     if (c->d_sched) cudaFree(c->d_sched);
     if (c->d_pair) cudaFree(c->d_pair);
+    if (c->d_wave) cudaFree(c->d_wave);
     if (c->gcol) cudaFree(c->gcol);
     if (c->grow) cudaFree(c->grow);
     for (auto& t : c->tev) {
@@ -1097,6 +1163,19 @@ int hftw_step(hftw_ctx* c, int64_t nsteps) {
             c->step_count += 2;
         }
         nsteps -= 2 * pairs;
+    }
+    if (k == HFTW_KERNEL_FUSED_TMA && c->wave_ok && nsteps >= 2 && c->tma_ok) {
+        // all steps in one persistent launch (weather_wave.cuh); chunks of
+        // at most 2^20 steps keep the work-list index in an int
+        while (nsteps > 0) {
+            const int64_t n = std::min<int64_t>(nsteps, (int64_t)1 << 20);
+            if (n < 2) break;
+            if ((rc = launch_wave(c, c->cur, n))) return rc;
+            if (n & 1) c->cur ^= 1;
+            c->step_count += n;
+            c->eu_derived = true;
+            nsteps -= n;
+        }
     }
     const int k1 = k == HFTW_KERNEL_FUSED_PAIR ? HFTW_KERNEL_FUSED_TMA : k;
     for (int64_t s = 0; s < nsteps; ++s) {

@@ -57,12 +57,15 @@ __device__ __forceinline__ double phys(double ev, int k, int nz, double sfv, dou
     return p;
 }
 
-template <bool PHYS>
+// COHERENT: e is written by other CTAs during the launch (the multi-step
+// kernel), so it is read through L2 (ld.global.cg), never the read-only path.
+template <bool PHYS, bool COHERENT = false>
 __device__ __forceinline__ double P_at(const double* __restrict__ e,
                                        const double* __restrict__ sf,
                                        const double* __restrict__ pb, const Dom& d, int i, int j,
                                        int k) {
-    double ev = __ldg(e + i * d.si + j * d.sj + (long long)(k - 1) * d.sk);
+    const double* pe = e + i * d.si + j * d.sj + (long long)(k - 1) * d.sk;
+    double ev = COHERENT ? __ldcg(pe) : __ldg(pe);
     double sfv = 0.0, pbv = 0.0;
     if (PHYS && k == 1) sfv = __ldg(sf + i + j * d.s2j);
     if (PHYS && k == d.nz) pbv = __ldg(pb + i + j * d.s2j);
@@ -71,38 +74,38 @@ __device__ __forceinline__ double P_at(const double* __restrict__ e,
 
 // New value of one owned cell, in the reference's region precedence
 // (i ghosts win over j ghosts, which win over the k planes).
-template <bool PHYS>
+template <bool PHYS, bool COHERENT = false>
 __device__ __forceinline__ double cell_update(const double* __restrict__ e,
                                               const double* __restrict__ sf,
                                               const double* __restrict__ pb, const Dom& d, int i,
                                               int j, int k) {
     if ((d.own_w && i == 0) || (d.own_e && i == d.nx + 1)) {
         // weather.cpp:164-167: (1-2dv)*e(i) + dv*(e(1) + e(nx))
-        double a = P_at<PHYS>(e, sf, pb, d, i == 0 ? 1 : d.efar, j, k);
-        double b = P_at<PHYS>(e, sf, pb, d, i == 0 ? d.wfar : d.nx, j, k);
-        return dadd(dmul(d.c2, P_at<PHYS>(e, sf, pb, d, i, j, k)), dmul(d.dv, dadd(a, b)));
+        double a = P_at<PHYS, COHERENT>(e, sf, pb, d, i == 0 ? 1 : d.efar, j, k);
+        double b = P_at<PHYS, COHERENT>(e, sf, pb, d, i == 0 ? d.wfar : d.nx, j, k);
+        return dadd(dmul(d.c2, P_at<PHYS, COHERENT>(e, sf, pb, d, i, j, k)), dmul(d.dv, dadd(a, b)));
     }
     if ((d.own_s && j == 0) || (d.own_n && j == d.ny + 1)) {
         // weather.cpp:155-158: (1-2dv)*e(j) + dv*(e(ny) + e(1))
-        double a = P_at<PHYS>(e, sf, pb, d, i, j == 0 ? d.sfar : d.ny, k);
-        double b = P_at<PHYS>(e, sf, pb, d, i, j == 0 ? 1 : d.nfar, k);
-        return dadd(dmul(d.c2, P_at<PHYS>(e, sf, pb, d, i, j, k)), dmul(d.dv, dadd(a, b)));
+        double a = P_at<PHYS, COHERENT>(e, sf, pb, d, i, j == 0 ? d.sfar : d.ny, k);
+        double b = P_at<PHYS, COHERENT>(e, sf, pb, d, i, j == 0 ? 1 : d.nfar, k);
+        return dadd(dmul(d.c2, P_at<PHYS, COHERENT>(e, sf, pb, d, i, j, k)), dmul(d.dv, dadd(a, b)));
     }
-    double c = P_at<PHYS>(e, sf, pb, d, i, j, k);
-    double s = dadd(P_at<PHYS>(e, sf, pb, d, i - 1, j, k), P_at<PHYS>(e, sf, pb, d, i + 1, j, k));
-    s = dadd(s, P_at<PHYS>(e, sf, pb, d, i, j - 1, k));
-    s = dadd(s, P_at<PHYS>(e, sf, pb, d, i, j + 1, k));
+    double c = P_at<PHYS, COHERENT>(e, sf, pb, d, i, j, k);
+    double s = dadd(P_at<PHYS, COHERENT>(e, sf, pb, d, i - 1, j, k), P_at<PHYS, COHERENT>(e, sf, pb, d, i + 1, j, k));
+    s = dadd(s, P_at<PHYS, COHERENT>(e, sf, pb, d, i, j - 1, k));
+    s = dadd(s, P_at<PHYS, COHERENT>(e, sf, pb, d, i, j + 1, k));
     if (k == 1) { // weather.cpp:142-145
-        s = dadd(s, P_at<PHYS>(e, sf, pb, d, i, j, 2));
+        s = dadd(s, P_at<PHYS, COHERENT>(e, sf, pb, d, i, j, 2));
         return dadd(dmul(d.c5, c), dmul(d.dv, s));
     }
     if (k == d.nz) { // weather.cpp:146-149
-        s = dadd(s, P_at<PHYS>(e, sf, pb, d, i, j, d.nz - 1));
+        s = dadd(s, P_at<PHYS, COHERENT>(e, sf, pb, d, i, j, d.nz - 1));
         return dadd(dmul(d.c5, c), dmul(d.dv, s));
     }
     // weather.cpp:134-137
-    s = dadd(s, P_at<PHYS>(e, sf, pb, d, i, j, k - 1));
-    s = dadd(s, P_at<PHYS>(e, sf, pb, d, i, j, k + 1));
+    s = dadd(s, P_at<PHYS, COHERENT>(e, sf, pb, d, i, j, k - 1));
+    s = dadd(s, P_at<PHYS, COHERENT>(e, sf, pb, d, i, j, k + 1));
     return dadd(dmul(d.c6, c), dmul(d.dv, s));
 }
 

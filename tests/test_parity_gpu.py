@@ -285,3 +285,34 @@ def test_pair_kernel_asuca_vs_oracle(coracle):
         ctx.step(5)
         for f in ("energy", "energy_u"):
             assert np.array_equal(ctx.download(f), getattr(want, f)), f
+
+
+@pytest.mark.parametrize("shape,steps", [((200, 300, 20), 13), ((130, 70, 58), 7),
+                                         ((64, 64, 2), 5), ((65, 129, 9), 4), ((3, 200, 5), 6),
+                                         ((129, 65, 58), 2)])
+def test_multi_step_launch_vs_oracle(coracle, shape, steps):
+    """hftw_step(n >= 2) runs all n steps in one persistent launch (per-chunk
+    dependency counters, ghost-row tasks): bitwise against the oracle, including
+    grids of one chunk (first == last) and a short last chunk, and a second call
+    on the same context (the counters re-arm themselves)."""
+    nx, ny, nz = shape
+    rng = np.random.default_rng(3 * nx + 5 * ny + nz + steps)
+    cfg = W.GridConfig(nx=nx, ny=ny, nz=nz, diffusion_velocity=float(rng.uniform(0, 1 / 6)),
+                       radiation_intensity=float(rng.uniform(-0.5, 0.5)),
+                       transfer_velocity=float(rng.uniform(0, 0.1)))
+    g = O.grid_from(cfg)
+    n3, n2 = O.shapes(g)
+    s0 = O.State(rng.uniform(150, 350, n3), rng.uniform(150, 350, n3),
+                 rng.uniform(150, 350, n2), rng.uniform(150, 350, n2))
+    want = coracle.steps(g, s0, 2 * steps).fields()
+    with W.Context(cfg) as ctx:
+        assert ctx.kernel == "fused_tma"
+        for name, arr in s0.fields().items():
+            ctx.upload(name, np.ascontiguousarray(arr))
+        ctx.set_timing(True)
+        ctx.step(steps)
+        ctx.step(steps)
+        ms, n = ctx.timing(2)
+        assert n == 2  # both calls were single multi-step launches
+        got = {f: ctx.download(f) for f in ("energy", "energy_u", "energy_surf", "energy_pbl")}
+    assert_same(got, want, f"{shape}/wave/{steps}")

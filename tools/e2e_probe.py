@@ -1,7 +1,6 @@
-"""e2e probe: hftw_step_host time vs row-block count, and its PCIe legs alone."""
+"""e2e probe: hftw_step_host time per PCIe copy mode (2D per row block vs nz 1D copies)."""
 import os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np
 import torch
 from paper_1802_05839_b200 import weather as W
 
@@ -14,12 +13,12 @@ with W.Context(cfg) as ctx:
     ctx.init()
     for name, a in (("energy", e), ("energy_surf", sf), ("energy_pbl", pb)):
         ctx.download(name, a)
-    for skip in (0, 1, 2):
-        os.environ["HFTW_PIPE_SKIP"] = str(skip)
-        for nb in (32,):
-            os.environ["HFTW_PIPE_BLOCKS"] = str(nb)
+    for mode in ("0",):
+        for skip in ("0", "1", "2"):
+            os.environ["HFTW_PIPE_1D"] = mode
+            os.environ["HFTW_PIPE_SKIP"] = skip
             ctx.step_host(e, sf, pb, e, eu)
             t0 = time.perf_counter()
             for _ in range(3):
                 ctx.step_host(e, sf, pb, e, eu)
-            print(f"skip {skip} blocks {nb}: {(time.perf_counter() - t0) / 3 * 1e3:.1f} ms/step_host", flush=True)
+            print(f"1d={mode} skip={skip}: {(time.perf_counter() - t0) / 3 * 1e3:.1f} ms", flush=True)
