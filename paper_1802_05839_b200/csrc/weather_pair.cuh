@@ -325,31 +325,31 @@ __device__ __forceinline__ void row_fast(const IRow& r, double* P0, double* P1, 
     for (int kk = 0; kk < NK; ++kk) qi[kk * kPairIC] = P2[kk];
 }
 
-// Row j of e_{s+2} from the three intermediate row buffers (Bm = row j-1,
-// B0 = row j, Bp = row j+1) at the thread's column: weather.cpp:130-150 on P'.
+// Row j of e_{s+2}: the i neighbours from the row buffer of row j (B0), the
+// j-1 neighbour from the buffer of row j-1 (Bm), and the centre, its k
+// neighbours and the j+1 neighbour from registers (Pc = row j, Pn = row j+1,
+// both this thread's column); only the k neighbours across the group's ends
+// come from B0.  weather.cpp:130-150 on P'.
 template <int NK, bool FIRST, bool LAST>
-__device__ __forceinline__ void final_smem(const double* Bm, const double* B0, const double* Bp,
-                                           double* q, long long sk, int kl, bool store,
-                                           const Dom& d) {
+__device__ __forceinline__ void final_smem(const double* Bm, const double* B0, const double* Pc,
+                                           const double* Pn, double* q, long long sk, int kl,
+                                           bool store, const Dom& d) {
     const double dv = d.dv, c6 = d.c6, c5 = d.c5;
     const int o0 = (kl - 1) * kPairIC;
     Bm += o0;
     B0 += o0;
-    Bp += o0;
     double v[NK];
 #pragma unroll
     for (int kk = 0; kk < NK; ++kk) {
         const int o = kk * kPairIC;
         double s = dadd(B0[o - 1], B0[o + 1]);
         s = dadd(s, Bm[o]);
-        s = dadd(s, Bp[o]);
-        const double pc = B0[o];
-        if (FIRST && kk == 0) v[kk] = dadd(dmul(c5, pc), dmul(dv, dadd(s, B0[o + kPairIC])));
-        else if (LAST && kk == NK - 1)
-            v[kk] = dadd(dmul(c5, pc), dmul(dv, dadd(s, B0[o - kPairIC])));
-        else
-            v[kk] = dadd(dmul(c6, pc),
-                         dmul(dv, dadd(dadd(s, B0[o - kPairIC]), B0[o + kPairIC])));
+        s = dadd(s, Pn[kk]);
+        const double km = kk > 0 ? Pc[kk - 1] : (FIRST ? 0.0 : B0[o - kPairIC]);
+        const double kp = kk + 1 < NK ? Pc[kk + 1] : (LAST ? 0.0 : B0[o + kPairIC]);
+        if (FIRST && kk == 0) v[kk] = dadd(dmul(c5, Pc[kk]), dmul(dv, dadd(s, kp)));
+        else if (LAST && kk == NK - 1) v[kk] = dadd(dmul(c5, Pc[kk]), dmul(dv, dadd(s, km)));
+        else v[kk] = dadd(dmul(c6, Pc[kk]), dmul(dv, dadd(dadd(s, km), kp)));
     }
     if (store) {
 #pragma unroll
@@ -572,7 +572,8 @@ __global__ void __launch_bounds__(kPairThreads, 1)
     int shape = nz < 2 * kPairKG || fl == 3 ? 16
                 : nk == KPT ? fl : nk == KPT - 1 ? 4 + fl : nk == KPT - 2 ? 8 + fl : 16;
 
-    double PW2[KPT]; // this row's intermediate values (for publication)
+    double PW2[KPT]; // this row's intermediate values
+    double PW1[KPT]; // the previous row's (the final row's centre)
     RingPos R0{0, 0}; // ring position of the current unit's first slab (row ja-2)
     int ibi = 0;      // row buffer of the next intermediate row (rotates over 3)
     for (;;) {
@@ -647,16 +648,18 @@ __global__ void __launch_bounds__(kPairThreads, 1)
                 double* q = u + (long long)gi * d.si + (long long)(jr - 1) * d.sj +
                             (long long)(kl - 1) * d.sk;
                 switch (shape) {
-                case 0: final_smem<KPT, false, false>(Bm, B0, Bp, q, d.sk, kl, true, d); break;
-                case 1: final_smem<KPT, true, false>(Bm, B0, Bp, q, d.sk, kl, true, d); break;
-                case 2: final_smem<KPT, false, true>(Bm, B0, Bp, q, d.sk, kl, true, d); break;
-                case 4: final_smem<KPT - 1, false, false>(Bm, B0, Bp, q, d.sk, kl, true, d); break;
-                case 5: final_smem<KPT - 1, true, false>(Bm, B0, Bp, q, d.sk, kl, true, d); break;
-                case 6: final_smem<KPT - 1, false, true>(Bm, B0, Bp, q, d.sk, kl, true, d); break;
+                case 0: final_smem<KPT, false, false>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d); break;
+                case 1: final_smem<KPT, true, false>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d); break;
+                case 2: final_smem<KPT, false, true>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d); break;
+                case 4: final_smem<KPT - 1, false, false>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d); break;
+                case 5: final_smem<KPT - 1, true, false>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d); break;
+                case 6: final_smem<KPT - 1, false, true>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d); break;
                 default: final_smem_generic<KPT>(Bm, B0, Bp, q, d.sk, kl, nk, d); break;
                 }
             }
             __syncthreads(); // the final row is done reading buffer ib2 (next row's target)
+#pragma unroll
+            for (int kk = 0; kk < KPT; ++kk) PW1[kk] = PW2[kk];
             ibi = ibi == 2 ? 0 : ibi + 1;
             Ra = Rb;
             Rb = Rc;
