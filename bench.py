@@ -342,7 +342,8 @@ def run_ours(args):
         alg_bytes = kinds[dom]["algorithmic_bytes_per_launch"]
         dom_name = {"pair": "fused_pair", "multi_step": "fused_tma_multistep"}.get(
             dom, "fused_tma" if kernel_name == "fused_pair" else kernel_name)
-        launches = sum(k["launches"] for k in kinds.values())
+        launches = sum(k["launches"] * (ctx.launches_per_step if n == "single_step" else 1)
+                       for n, k in kinds.items())
     else:
         dom, dom_name = None, kernel_name
         avg_launch_s = statistics.mean(launch_ms) * 1e-3

@@ -1179,6 +1179,9 @@ int hftw_step(hftw_ctx* c, int64_t nsteps) {
     }
     const int k1 = k == HFTW_KERNEL_FUSED_PAIR ? HFTW_KERNEL_FUSED_TMA : k;
     for (int64_t s = 0; s < nsteps; ++s) {
+        if (k == HFTW_KERNEL_SPLIT || k == HFTW_KERNEL_FUSED_CELL) {
+            if ((rc = timing_mark(c, 0, true))) return rc;
+        }
         if (k == HFTW_KERNEL_SPLIT) {
             // the reference's structure: physics in place, then diffusion
             if ((rc = launch_physics(c, c->cur, 0))) return rc;
@@ -1187,11 +1190,11 @@ int hftw_step(hftw_ctx* c, int64_t nsteps) {
                 return rc;
             c->eu_derived = false;
         } else {
-            if ((rc = timing_mark(c, 0, true))) return rc;
+            if (k1 != HFTW_KERNEL_FUSED_CELL && (rc = timing_mark(c, 0, true))) return rc;
             if ((rc = launch_fused<true>(c, c->cur, k1))) return rc;
-            if ((rc = timing_mark(c, 0, false))) return rc;
             c->eu_derived = true;
         }
+        if ((rc = timing_mark(c, 0, false))) return rc;
         c->cur ^= 1;
         ++c->step_count;
     }

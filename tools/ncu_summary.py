@@ -59,6 +59,8 @@ def main():
     ap.add_argument("--key")
     ap.add_argument("--alg-bytes", type=float)
     ap.add_argument("--note", default="")
+    ap.add_argument("--steps-per-launch", type=float, default=1.0,
+                    help="a multi-step launch: ncu_traffic.json stores the traffic per step")
     a = ap.parse_args()
     L = raw(a.rep)
     summ = []
@@ -92,7 +94,7 @@ def main():
     if a.key and summ and summ[0].get("dram_bytes_total"):
         path = os.path.join(os.path.dirname(a.out) or ".", "ncu_traffic.json")
         d = json.load(open(path)) if os.path.exists(path) else {}
-        d[a.key] = summ[0]["dram_bytes_total"]
+        d[a.key] = summ[0]["dram_bytes_total"] / a.steps_per_launch
         json.dump(d, open(path, "w"), indent=1, sort_keys=True)
     print(json.dumps(summ[0], indent=1))
 
