@@ -114,7 +114,7 @@ struct hftw_ctx {
 
     // pair kernel (two steps per pass; single-domain IJK, nz <= 64)
     bool pair_ok = false;
-    bool pair_auto = false;     // AUTO keeps the single-step kernel (pair kernel)
+    bool pair_auto = env_int("HFTW_NO_PAIR", 0) == 0; // AUTO: two-step passes where available
     int pair_ns = 0, pair_chunk = 0, pair_nchunks = 0, pair_ctas = 0;
     size_t pair_smem = 0;
     CUtensorMap tm_e2[2]{};             // e: slab boxes {kPairW, 1, nz}
@@ -428,8 +428,14 @@ int setup_pair(hftw_ctx* c) {
     CUDA_TRY(c, cudaFuncGetAttributes(&fa, kern));
     const int nz = (int)c->nz;
     int ns = 0;
+    // narrow tiles: the deepest ring that still lets kPairMinBlocks CTAs share an SM
+    int smem_sm = 0;
+    CUDA_TRY(c, cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor,
+                                       c->device));
+    const size_t per_cta = std::min<size_t>((size_t)smem_optin,
+                                            (size_t)smem_sm / hftw::kPairMinBlocks - 1024);
     for (int cand = std::min(8, env_int("HFTW_PAIR_NS", 8)); cand >= 4; --cand)
-        if (hftw::pair_smem_bytes(nz, cand) + fa.sharedSizeBytes <= (size_t)smem_optin) {
+        if (hftw::pair_smem_bytes(nz, cand) + fa.sharedSizeBytes <= per_cta) {
             ns = cand;
             break;
         }
@@ -480,9 +486,9 @@ int setup_pair(hftw_ctx* c) {
     const long long slots = (long long)per_sm * c->num_sms;
     if (chunk <= 0) {
         double best = 1e30;
-        // (measured at ASUCA size: 24-row units beat longer ones, whose tail
+        // (measured at ASUCA size: 16-row units beat longer ones, whose tail
         // at the end of the launch costs more than their halo rows save)
-        for (long long ch = std::min<long long>(24, ny); ch >= 1; --ch) {
+        for (long long ch = std::min<long long>(16, ny); ch >= 1; --ch) {
             const long long units = (long long)c->pair_nstrips * ((ny + ch - 1) / ch);
             const double waves = (double)((units + slots - 1) / slots);
             const double cost = waves * (double)(ch + 4);
@@ -596,6 +602,7 @@ int launch_wave(hftw_ctx* c, int src, int64_t nsteps) {
     a.ns = c->ns;
     a.nsteps = (int)nsteps;
     a.gtasks = c->wave_gtasks;
+    a.alt = env_int("HFTW_WAVE_ALT", 1);
     a.sched = c->d_wave;
     a.chunk_done = c->d_wave + 2;
     a.ghost_done = c->d_wave + 2 + c->wave_nchunks;
@@ -1164,7 +1171,8 @@ int hftw_step(hftw_ctx* c, int64_t nsteps) {
         }
         nsteps -= 2 * pairs;
     }
-    if (k == HFTW_KERNEL_FUSED_TMA && c->wave_ok && nsteps >= 2 && c->tma_ok) {
+    if ((k == HFTW_KERNEL_FUSED_TMA || k == HFTW_KERNEL_FUSED_PAIR) && c->wave_ok &&
+        nsteps >= 2 && c->tma_ok) {
         // all steps in one persistent launch (weather_wave.cuh); chunks of
         // at most 2^20 steps keep the work-list index in an int
         while (nsteps > 0) {

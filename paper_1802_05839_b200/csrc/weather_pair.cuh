@@ -36,14 +36,18 @@
 
 namespace hftw {
 
-constexpr int kPairTX = 62;                     // output columns per strip
-constexpr int kPairIC = kPairTX + 2;            // intermediate columns i0-1 .. i0+62 (2 warps)
+#ifndef HFTW_PAIR_TX
+#define HFTW_PAIR_TX 30
+#endif
+constexpr int kPairTX = HFTW_PAIR_TX;           // output columns per strip (30: 2 CTAs per SM)
+constexpr int kPairIC = kPairTX + 2;            // intermediate columns i0-1 .. i0+TX (warps)
 constexpr int kPairW = kPairTX + 4;             // slab columns i0-2 .. i0+63
 #ifndef HFTW_PAIR_KG
 #define HFTW_PAIR_KG 8
 #endif
 constexpr int kPairKG = HFTW_PAIR_KG;           // k-groups (8: 512 threads, <= 8 planes each)
 constexpr int kPairThreads = kPairIC * kPairKG;
+constexpr int kPairMinBlocks = kPairThreads <= 256 ? 2 : 1; // CTAs per SM the tile allows
 constexpr int kPairNIB = 3;                     // intermediate row buffers (rows j-1, j, j+1)
 
 __host__ __device__ inline int round128(int b) { return (b + 127) / 128 * 128; }
@@ -530,7 +534,7 @@ struct RingPos {
 
 // KPT: max k planes per thread (nz <= 8 * KPT).
 template <int KPT>
-__global__ void __launch_bounds__(kPairThreads, 1)
+__global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
     step_pair_kernel(const __grid_constant__ CUtensorMap tm_e,
                      const __grid_constant__ CUtensorMap tm_sfpb,
                      const __grid_constant__ CUtensorMap tm_ef,

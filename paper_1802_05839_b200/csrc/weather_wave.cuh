@@ -43,6 +43,7 @@ struct WaveArgs {
     int nstrips, nchunks, chunk, ns;
     int nsteps;          // steps of this launch
     int gtasks;          // ghost-row tasks per step
+    int alt;             // odd chunks sweep their rows downwards (see wave_rows_down)
     int* sched;          // [0] next work item, [1] CTAs finished
     int* chunk_done;     // [nchunks] units completed (all steps of this launch)
     int* ghost_done;     // [1] ghost-row tasks completed
@@ -57,6 +58,10 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
 }
 __device__ __forceinline__ void wait_geq(const int* p, int target) {
     while (ld_acquire_gpu(p) < target) __nanosleep(100);
+}
+
+__device__ __forceinline__ bool wave_rows_down(const WaveArgs& a, int unit) {
+    return a.alt && ((unit / a.nstrips) & 1);
 }
 
 // One ghost-row task: its share of rows j = 0 and ny+1 (all i, corners
@@ -149,14 +154,17 @@ __device__ __forceinline__ void wave_consumers(unsigned char* smem, const SlabGe
         const int ja = ch * a.chunk + 1, jb = min(d.ny, ja + a.chunk - 1);
         const int i0 = 1 + st * TX;
         const bool active = c < min(TX, d.nx - i0 + 1) && kl <= kh;
-        for (int j = ja; j <= jb; ++j) {
-            const uint32_t l0 = L + (j - ja), l1 = l0 + 1, l2 = l0 + 2;
-            if (j == ja) mbar_wait(&full[l1 % NS], (l1 / NS) & 1);
+        const bool down = wave_rows_down(a, unit);
+        for (int m = 0; m <= jb - ja; ++m) {
+            // slabs l0, l1, l2 hold rows j-1, j, j+1 (upwards) or j+1, j, j-1 (downwards)
+            const int j = down ? jb - m : ja + m;
+            const uint32_t l0 = L + m, l1 = l0 + 1, l2 = l0 + 2;
+            if (m == 0) mbar_wait(&full[l1 % NS], (l1 / NS) & 1);
             mbar_wait(&full[l2 % NS], (l2 / NS) & 1);
             if (active) {
-                const unsigned char* stm = smem + (size_t)(l0 % NS) * G.stage;
+                const unsigned char* stm = smem + (size_t)((down ? l2 : l0) % NS) * G.stage;
                 const unsigned char* st0 = smem + (size_t)(l1 % NS) * G.stage;
-                const unsigned char* stp = smem + (size_t)(l2 % NS) * G.stage;
+                const unsigned char* stp = smem + (size_t)((down ? l0 : l2) % NS) * G.stage;
                 const double* em = reinterpret_cast<const double*>(stm) + cc;
                 const double* e0 = reinterpret_cast<const double*>(st0) + cc;
                 const double* ep = reinterpret_cast<const double*>(stp) + cc;
@@ -261,7 +269,12 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
                 }
                 const bool cmd = stop || r < a.gtasks; // a slot without data
                 const CUtensorMap* tm = (s & 1) ? &tm_e1 : &tm_e0;
-                for (int jj = ja - 1; cmd ? jj == ja - 1 : jj <= jb + 1; ++jj, ++L) {
+                // odd chunks load (and compute) their rows bottom-up: the rows two
+                // neighbouring chunks share are then read by both at about the same
+                // time (both units' starts, or both ends), while L2 still holds them
+                const bool down = !cmd && wave_rows_down(a, r - a.gtasks);
+                for (int t = 0; cmd ? t == 0 : t <= jb - ja + 2; ++t, ++L) {
+                    const int jj = down ? jb + 1 - t : ja - 1 + t;
                     const uint32_t slot = L % NS;
                     if (L >= (uint32_t)NS) mbar_wait(&empty[slot], ((L / NS) - 1) & 1);
                     slot_item[slot] = stop ? -1 : item;

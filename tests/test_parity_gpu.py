@@ -18,7 +18,7 @@ pytestmark = pytest.mark.gpu
 
 TOL = 0.0  # bitwise
 LAYOUTS = ["ijk", "kij"]
-KERNELS = ["auto", "fused_pair", "fused_cell", "split"]  # auto = the TMA kernel where it fits
+KERNELS = ["auto", "fused_tma", "fused_pair", "fused_cell", "split"]  # auto: pair (IJK) / TMA
 
 
 def cfg_of(d):
@@ -71,9 +71,9 @@ def test_golden_cases(golden, layout, kernel):
 
 @pytest.mark.parametrize("layout", LAYOUTS)
 def test_auto_kernel_selected(layout):
-    # AUTO: the single-step TMA kernel (the pair kernel is opt-in)
+    # AUTO: two-step passes (IJK, one domain, nz <= 60); the TMA kernel otherwise
     with W.Context(W.GridConfig(nx=100, ny=40, nz=58), layout=layout) as ctx:
-        assert ctx.kernel == "fused_tma"
+        assert ctx.kernel == ("fused_pair" if layout == "ijk" else "fused_tma")
         assert ctx.launches_per_step == 1
 
 
@@ -305,8 +305,7 @@ def test_multi_step_launch_vs_oracle(coracle, shape, steps):
     s0 = O.State(rng.uniform(150, 350, n3), rng.uniform(150, 350, n3),
                  rng.uniform(150, 350, n2), rng.uniform(150, 350, n2))
     want = coracle.steps(g, s0, 2 * steps).fields()
-    with W.Context(cfg) as ctx:
-        assert ctx.kernel == "fused_tma"
+    with W.Context(cfg, kernel="fused_tma") as ctx:
         for name, arr in s0.fields().items():
             ctx.upload(name, np.ascontiguousarray(arr))
         ctx.set_timing(True)
