@@ -116,6 +116,7 @@ struct hftw_ctx {
     bool pair_ok = false;
     bool pair_auto = env_int("HFTW_NO_PAIR", 0) == 0; // AUTO: two-step passes where available
     int pair_ns = 0, pair_chunk = 0, pair_nchunks = 0, pair_ctas = 0;
+    int pair_nbig = 0, pair_chunk2 = 0;
     size_t pair_smem = 0;
     CUtensorMap tm_e2[2]{};             // e: slab boxes {kPairW, 1, nz}
     CUtensorMap tm_ef[2]{};             // e: 2-wide far-column boxes
@@ -499,7 +500,13 @@ int setup_pair(hftw_ctx* c) {
         }
     }
     c->pair_chunk = (int)std::min<long long>(chunk, ny);
-    c->pair_nchunks = (int)((ny + c->pair_chunk - 1) / c->pair_chunk);
+    // the last ~1.5 waves of units get half-height chunks (a shorter tail)
+    c->pair_chunk2 = std::max(1, env_int("HFTW_PAIR_CHUNK2", (c->pair_chunk + 1) / 2));
+    const long long tail_rows = std::min<long long>(
+        ny, ((3 * slots / 2 + c->pair_nstrips - 1) / c->pair_nstrips) * c->pair_chunk2);
+    c->pair_nbig = (int)((ny - tail_rows) / c->pair_chunk);
+    const long long rest = ny - (long long)c->pair_nbig * c->pair_chunk;
+    c->pair_nchunks = c->pair_nbig + (int)((rest + c->pair_chunk2 - 1) / c->pair_chunk2);
     const long long units = (long long)c->pair_nstrips * c->pair_nchunks;
     c->pair_ctas = (int)std::min<long long>(slots, units);
     const size_t ints = 2 + (size_t)c->pair_nchunks + (size_t)c->pair_nstrips;
@@ -542,6 +549,8 @@ int launch_pair(hftw_ctx* c, int src) {
     a.nstrips = c->pair_nstrips;
     a.nchunks = c->pair_nchunks;
     a.chunk = c->pair_chunk;
+    a.nbig = c->pair_nbig;
+    a.chunk2 = c->pair_chunk2;
     a.ns = c->pair_ns;
     a.sched = c->d_pair;
     a.cnt_col = c->d_pair + 2;

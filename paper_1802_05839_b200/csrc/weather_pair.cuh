@@ -84,12 +84,21 @@ struct PairArgs {
     int fp;       // tensor-map i coordinate of logical i = 0
     int jrow0;    // tensor-map row coordinate of logical j = 0
     int nstrips, nchunks, chunk, ns;
+    int nbig;     // chunks 0 .. nbig-1 have `chunk` rows, the rest `chunk2` (the last
+    int chunk2;   // ~1.5 waves of units are shorter, so the launch's tail is shorter)
     int* sched;   // [0] next unit, [1] CTAs finished (self-resetting)
     int* cnt_col; // [nchunks] i-ghost producers done (strip 0 + last strip), self-resetting
     int* cnt_row; // [nstrips] j-ghost producers done (chunk 0 + last chunk), self-resetting
     double* gcol; // P' at i = 0, 1, nx, nx+1: [4][ny+2][nz]
     double* grow; // P' at j = 0, 1, ny, ny+1: [4][nz][nx+2]
 };
+
+// Rows ja..jb of chunk ch.
+__host__ __device__ inline void pair_rows(const PairArgs& a, int ny, int ch, int& ja, int& jb) {
+    ja = ch < a.nbig ? ch * a.chunk + 1 : a.nbig * a.chunk + (ch - a.nbig) * a.chunk2 + 1;
+    jb = ja + (ch < a.nbig ? a.chunk : a.chunk2) - 1;
+    if (jb > ny) jb = ny;
+}
 
 // Which cyclic partner column a unit's far TMA box holds (0 = none).
 __host__ __device__ inline int pair_far_col(int st, int nstrips, int nx) {
@@ -503,8 +512,9 @@ __device__ __forceinline__ void pair_issue(PairProducer& p, unsigned char* smem,
             return;
         }
         const int ch = p.unit / a.nstrips;
-        p.row = ch * a.chunk - 1; // ja - 2
-        p.jb = min(ny, ch * a.chunk + a.chunk);
+        int ja;
+        pair_rows(a, ny, ch, ja, p.jb);
+        p.row = ja - 2;
     }
     const int st = p.unit % a.nstrips;
     const int ic = a.fp + 1 + st * kPairTX - 2; // tensor i of i0 - 2 (even)
@@ -585,7 +595,8 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
         const int unit = slot_unit[R0.slot];
         if (unit < 0) break;
         const int ch = unit / a.nstrips, st = unit % a.nstrips;
-        const int ja = ch * a.chunk + 1, jb = min(ny, ja + a.chunk - 1);
+        int ja, jb;
+        pair_rows(a, ny, ch, ja, jb);
         const int i0 = 1 + st * kPairTX;
         const int gi = i0 - 2 + cc; // logical i of my intermediate column
         const bool indom = gi <= nx + 1 && nk > 0;
