@@ -48,7 +48,12 @@ constexpr int kPairW = kPairTX + 4;             // slab columns i0-2 .. i0+63
 constexpr int kPairKG = HFTW_PAIR_KG;           // k-groups (8: 512 threads, <= 8 planes each)
 constexpr int kPairThreads = kPairIC * kPairKG;
 constexpr int kPairMinBlocks = kPairThreads <= 256 ? 2 : 1; // CTAs per SM the tile allows
-constexpr int kPairNIB = 3;                     // intermediate row buffers (rows j-1, j, j+1)
+#ifndef HFTW_PAIR_NIB
+#define HFTW_PAIR_NIB 3
+#endif
+// intermediate row buffers: 3 (rows j-1, j, j+1; two barriers per row) or 4 (one
+// barrier per row: the buffer a row overwrites was last read two rows earlier)
+constexpr int kPairNIB = HFTW_PAIR_NIB;
 
 __host__ __device__ inline int round128(int b) { return (b + 127) / 128 * 128; }
 
@@ -589,7 +594,7 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
     double PW2[KPT]; // this row's intermediate values
     double PW1[KPT]; // the previous row's (the final row's centre)
     RingPos R0{0, 0}; // ring position of the current unit's first slab (row ja-2)
-    int ibi = 0;      // row buffer of the next intermediate row (rotates over 3)
+    int ibi = 0;      // row buffer of the next intermediate row (rotates over kPairNIB)
     for (;;) {
         mbar_wait(&full[R0.slot], R0.par);
         const int unit = slot_unit[R0.slot];
@@ -611,8 +616,9 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
         mbar_wait(&full[Rb.slot], Rb.par);
         for (int jr = ja - 1; jr <= jb + 1; ++jr) {
             mbar_wait(&full[Rc.slot], Rc.par);
-            // row buffers: jr -> ibi, jr-1 -> ibi-1, jr-2 -> ibi-2 (mod 3)
-            const int ib1 = ibi == 0 ? 2 : ibi - 1, ib2 = ib1 == 0 ? 2 : ib1 - 1;
+            // row buffers: jr -> ibi, jr-1 -> ibi-1, jr-2 -> ibi-2 (mod kPairNIB)
+            const int ib1 = ibi == 0 ? kPairNIB - 1 : ibi - 1;
+            const int ib2 = ib1 == 0 ? kPairNIB - 1 : ib1 - 1;
             double* ibrow = ib0 + ibi * ibn + (cc - 1);
             if (indom) {
                 const unsigned char* sm_ = smem + (size_t)Ra.slot * G.stage;
@@ -672,10 +678,11 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
                 default: final_smem_generic<KPT>(Bm, B0, Bp, q, d.sk, kl, nk, d); break;
                 }
             }
-            __syncthreads(); // the final row is done reading buffer ib2 (next row's target)
+            if (kPairNIB == 3)
+                __syncthreads(); // the final row is done reading buffer ib2 (next row's target)
 #pragma unroll
             for (int kk = 0; kk < KPT; ++kk) PW1[kk] = PW2[kk];
-            ibi = ibi == 2 ? 0 : ibi + 1;
+            ibi = ibi == kPairNIB - 1 ? 0 : ibi + 1;
             Ra = Rb;
             Rb = Rc;
             Rc = Rc.next(NS);
