@@ -46,6 +46,7 @@ constexpr int kFrontPad = 31; // IJK: logical i = 1 lands on a 256-byte boundary
 constexpr int kNCW = 16;      // consumer warps of the TMA kernel
 constexpr int kChunk = 32;    // rows per TMA work unit
 constexpr int kMaxPipeBlocks = 32; // row blocks of the hftw_step_host pipeline
+constexpr int kMaxWaveStepsDist = 1024; // steps per multi-step launch when decomposed
 #ifndef HFTW_PAIR_KPT
 #define HFTW_PAIR_KPT (64 / HFTW_PAIR_KG)
 #endif
@@ -571,7 +572,7 @@ int launch_pair(hftw_ctx* c, int src) {
 // domain, IJK, same slab ring as the single-step kernel.
 int setup_wave(hftw_ctx* c) {
     c->wave_ok = false;
-    if (!c->tma_ok || c->layout != HFTW_IJK || c->dist || c->tx != 64 || env_int("HFTW_NO_WAVE", 0))
+    if (!c->tma_ok || c->layout != HFTW_IJK || c->tx != 64 || env_int("HFTW_NO_WAVE", 0))
         return HFTW_OK;
     auto kern = hftw::step_wave_kernel<64, kNCW>;
     CUDA_TRY(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -592,7 +593,7 @@ int setup_wave(hftw_ctx* c) {
     c->wave_gtasks = std::max(1, std::min(16, (int)((c->lnx + 2) * c->nz / 2048)));
     const long long units = (long long)c->nstrips * c->wave_nchunks + c->wave_gtasks;
     c->wave_ctas = (int)std::min<long long>((long long)per_sm * c->num_sms, units);
-    const size_t ints = 2 + (size_t)c->wave_nchunks + 1;
+    const size_t ints = 2 + (size_t)c->wave_nchunks + 1 + kMaxWaveStepsDist;
     CUDA_TRY(c, cudaMalloc(&c->d_wave, ints * sizeof(int)));
     CUDA_TRY(c, cudaMemset(c->d_wave, 0, ints * sizeof(int)));
     c->wave_ok = true;
@@ -617,6 +618,9 @@ int launch_wave(hftw_ctx* c, int src, int64_t nsteps) {
     a.ghost_done = c->d_wave + 2 + c->wave_nchunks;
     a.buf0 = e3(c, src);
     a.buf1 = e3(c, src ^ 1);
+    a.h_even = make_halo(c, src ^ 1); // even steps write buf1
+    a.h_odd = make_halo(c, src);      // odd steps write buf0
+    a.step_done = c->d_wave + 2 + c->wave_nchunks + 1;
     int rc = timing_mark(c, 2, true);
     if (rc) return rc;
     hftw::step_wave_kernel<64, kNCW><<<c->wave_ctas, (kNCW + 1) * 32, c->smem, c->stream>>>(
@@ -1183,9 +1187,11 @@ int hftw_step(hftw_ctx* c, int64_t nsteps) {
     if ((k == HFTW_KERNEL_FUSED_TMA || k == HFTW_KERNEL_FUSED_PAIR) && c->wave_ok &&
         nsteps >= 2 && c->tma_ok) {
         // all steps in one persistent launch (weather_wave.cuh); chunks of
-        // at most 2^20 steps keep the work-list index in an int
+        // at most 2^20 steps keep the work-list index in an int (decomposed:
+        // kMaxWaveStepsDist, the per-step completion counters)
         while (nsteps > 0) {
-            const int64_t n = std::min<int64_t>(nsteps, (int64_t)1 << 20);
+            const int64_t n = std::min<int64_t>(
+                nsteps, c->dist ? (int64_t)kMaxWaveStepsDist : (int64_t)1 << 20);
             if (n < 2) break;
             if ((rc = launch_wave(c, c->cur, n))) return rc;
             if (n & 1) c->cur ^= 1;

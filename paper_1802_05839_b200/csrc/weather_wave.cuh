@@ -49,6 +49,11 @@ struct WaveArgs {
     int* ghost_done;     // [1] ghost-row tasks completed
     double* buf0;        // field of step 0 (logical (0,0,1)); steps alternate
     double* buf1;
+    // decomposed runs (Halo::active): the pushes of steps writing buf1 (even s) and
+    // buf0 (odd s), and per-step completion counters -- when the last work item of
+    // step s finishes, its thread publishes flag = h.step + s + 1 to the neighbours
+    Halo h_even, h_odd;
+    int* step_done;      // [nsteps]
 };
 
 __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
@@ -70,16 +75,24 @@ __device__ __forceinline__ void wave_ghost_rows(const double* __restrict__ e,
                                                 double* __restrict__ u,
                                                 const double* __restrict__ sf,
                                                 const double* __restrict__ pb, const Dom& d,
-                                                int task, int ntasks, int tid, int nthreads) {
-    const long long ni = d.nx + 2;
-    const long long n = 2 * ni * d.nz;
+                                                const Halo& h, int task, int ntasks, int tid,
+                                                int nthreads) {
+    // the rows this domain owns (a decomposed rank owns the global ghost row of
+    // its edge, if any), over its owned i range; cells next to a neighbour are
+    // pushed into its halo as in step_tma_kernel
+    const Owned o = owned(d);
+    const int rows = (d.own_s ? 1 : 0) + (d.own_n ? 1 : 0);
+    const long long ni = o.i1 - o.i0 + 1;
+    const long long n = rows * ni * d.nz;
     const long long lo = n * task / ntasks, hi = n * (task + 1) / ntasks;
     for (long long t = lo + tid; t < hi; t += nthreads) {
-        const int i = (int)(t % ni);
+        const int i = o.i0 + (int)(t % ni);
         const long long q = t / ni;
         const int k = 1 + (int)(q % d.nz);
-        const int j = (q / d.nz) == 0 ? 0 : d.ny + 1;
-        u[i * d.si + j * d.sj + (long long)(k - 1) * d.sk] = cell_update<true, true>(e, sf, pb, d, i, j, k);
+        const int j = ((q / d.nz) == 0 && d.own_s) ? 0 : d.ny + 1;
+        const double v = cell_update<true, true>(e, sf, pb, d, i, j, k);
+        u[i * d.si + j * d.sj + (long long)(k - 1) * d.sk] = v;
+        halo_push(h, d, i, j, k, v);
     }
 }
 
@@ -100,6 +113,19 @@ __device__ __forceinline__ void wave_ghost_cols(const double* __restrict__ e,
         const int k = 1 + (int)(q / nr);
         const int i = w ? 0 : d.nx + 1;
         u[i * d.si + j * d.sj + (long long)(k - 1) * d.sk] = cell_update<true, true>(e, sf, pb, d, i, j, k);
+    }
+}
+
+// A work item of step s is complete (its stores are issued): count it; the
+// thread completing the step publishes it to the neighbours (decomposed runs).
+__device__ __forceinline__ void wave_item_done(const WaveArgs& a, int s, int per_step) {
+    const Halo& h = (s & 1) ? a.h_odd : a.h_even;
+    if (!h.active) return;
+    __threadfence_system(); // this item's pushes into the neighbours precede the count
+    if (atomicAdd(&a.step_done[s], 1) == per_step - 1) {
+        __threadfence_system();
+        for (int dd = 0; dd < 4; ++dd)
+            if (h.nb[dd]) st_release_sys(&h.nb_flags[dd][dd ^ 1], (unsigned long long)(h.step + s + 1));
     }
 }
 
@@ -135,17 +161,20 @@ __device__ __forceinline__ void wave_consumers(unsigned char* smem, const SlabGe
         const int s = item / per_step, r = item % per_step;
         const double* e = (s & 1) ? a.buf1 : a.buf0;
         double* u = (s & 1) ? a.buf0 : a.buf1;
+        const Halo& hs = (s & 1) ? a.h_odd : a.h_even; // pushes of this step
         if (r < a.gtasks) {
             // ghost-row task: from global memory, no slab
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[L % NS]);
             ++L;
-            wave_ghost_rows(e, u, sf, pb, d, r, a.gtasks, tid, nthreads);
+            wave_ghost_rows(e, u, sf, pb, d, (s & 1) ? a.h_odd : a.h_even, r, a.gtasks, tid,
+                            nthreads);
             asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
             if (tid == 0) {
                 __threadfence();
                 asm volatile("fence.proxy.async.global;" ::: "memory");
                 atomicAdd(a.ghost_done, 1);
+                wave_item_done(a, s, per_step);
             }
             continue;
         }
@@ -178,7 +207,8 @@ __device__ __forceinline__ void wave_consumers(unsigned char* smem, const SlabGe
                              (long long)(kl - 1) * d.sk;
                 const ColumnRow row{em, e0, ep, Sm, S0, Sp, Bm, B0, Bp, up, d.sk,
                                     w, 1, kl, kh, nz, ri, tv, dv, c5, c6, i0 + c, j};
-                column_row<true, false>(row, noh, d);
+                if (hs.active) column_row<true, true>(row, hs, d);
+                else column_row<true, false>(row, noh, d);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[l0 % NS]);
@@ -191,7 +221,7 @@ __device__ __forceinline__ void wave_consumers(unsigned char* smem, const SlabGe
         }
         L = lend + 2;
         // the i-ghost columns of these rows (their partners are in the same rows)
-        const bool west = st == 0, east = st == a.nstrips - 1;
+        const bool west = st == 0 && d.own_w, east = st == a.nstrips - 1 && d.own_e;
         if (west || east) wave_ghost_cols(e, u, sf, pb, d, ja, jb, west, east, tid, nthreads);
         // publish: every consumer's stores of this unit precede the count
         asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
@@ -199,6 +229,7 @@ __device__ __forceinline__ void wave_consumers(unsigned char* smem, const SlabGe
             __threadfence();
             asm volatile("fence.proxy.async.global;" ::: "memory");
             atomicAdd(&a.chunk_done[ch], 1);
+            wave_item_done(a, s, per_step);
         }
     }
 }
@@ -244,11 +275,18 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
                     r = item % per_step;
                 }
                 // ghost-row task of step s: rows 0, 1, ny, ny+1 of step s-1 done
+                // (and, decomposed, the neighbours' step s-1: far slots, corners)
                 if (!stop && r < a.gtasks) {
                     if (s > 0) {
                         wait_geq(&a.chunk_done[0], s * a.nstrips);
                         wait_geq(&a.chunk_done[last], s * a.nstrips);
                         wait_geq(a.ghost_done, s * a.gtasks);
+                    }
+                    const Halo& hs = (s & 1) ? a.h_odd : a.h_even;
+                    if (hs.active) {
+                        Halo hw = hs;
+                        hw.step = hs.step + s;
+                        halo_wait(hw, 0xF);
                     }
                 }
                 int ja = 0, jb = -1, ic = 0;
@@ -263,6 +301,17 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
                         wait_geq(&a.chunk_done[ch], s * a.nstrips);
                         if (ch < last) wait_geq(&a.chunk_done[ch + 1], s * a.nstrips);
                         if (ch == 0 || ch == last) wait_geq(a.ghost_done, s * a.gtasks);
+                    }
+                    // decomposed: a unit on the subdomain rim reads halo slots the
+                    // neighbour pushed in its step s-1 and pushes into slots it read
+                    // then -- wait until that neighbour has finished step s-1
+                    const Halo& hs = (s & 1) ? a.h_odd : a.h_even;
+                    const int mask = (st == 0 ? 1 : 0) | (st == a.nstrips - 1 ? 2 : 0) |
+                                     (ch == 0 ? 4 : 0) | (ch == last ? 8 : 0);
+                    if (hs.active && mask) {
+                        Halo hw = hs;
+                        hw.step = hs.step + s;
+                        halo_wait(hw, mask);
                     }
                     // generic-proxy writes of other CTAs -> this CTA's TMA reads
                     asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -304,6 +353,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
         if (atomicAdd(&a.sched[1], 1) == (int)gridDim.x - 1) {
             for (int c = 0; c < a.nchunks; ++c) a.chunk_done[c] = 0;
             *a.ghost_done = 0;
+            if (a.h_even.active)
+                for (int t = 0; t < a.nsteps; ++t) a.step_done[t] = 0;
             a.sched[0] = 0;
             a.sched[1] = 0;
             __threadfence();

@@ -69,6 +69,9 @@ def _worker(rank, world, port, shape, grid, steps, layout, kernel, random_init, 
     ((66, 41, 9), (2, 2), 3, "kij", "auto", True),
     ((66, 41, 9), (2, 2), 3, "ijk", "fused_cell", False),
     ((130, 45, 7), (4, 2), 3, "ijk", "auto", True),
+    # multi-step launches with in-kernel pushes and per-step flags, many steps per call
+    ((131, 97, 12), (2, 2), 11, "ijk", "fused_tma", True),
+    ((200, 140, 20), (2, 4), 9, "ijk", "auto", True),
 ])
 def test_decomposed_gpu_bitwise(shape, grid, steps, layout, kernel, random_init):
     import torch.multiprocessing as mp
