@@ -118,6 +118,7 @@ struct hftw_ctx {
     bool pair_auto = env_int("HFTW_NO_PAIR", 0) == 0; // AUTO: two-step passes where available
     int pair_ns = 0, pair_chunk = 0, pair_nchunks = 0, pair_ctas = 0;
     int pair_nbig = 0, pair_chunk2 = 0;
+    bool pair_fast = false;     // every k-group has a compile-time row shape (AUTO uses it)
     size_t pair_smem = 0;
     CUtensorMap tm_e2[2]{};             // e: slab boxes {kPairW, 1, nz}
     CUtensorMap tm_ef[2]{};             // e: 2-wide far-column boxes
@@ -515,13 +516,16 @@ int setup_pair(hftw_ctx* c) {
     CUDA_TRY(c, cudaMemset(c->d_pair, 0, ints * sizeof(int)));
     CUDA_TRY(c, cudaMalloc(&c->gcol, (size_t)(4 * (ny + 2) * c->nz) * sizeof(double)));
     CUDA_TRY(c, cudaMalloc(&c->grow, (size_t)(4 * c->nz * (c->lnx + 2)) * sizeof(double)));
+    // the compile-time row shapes cover groups of KPT-2 .. KPT planes; other nz run
+    // the generic (runtime plane checks) path, which AUTO leaves to the TMA kernel
+    c->pair_fast = c->nz >= (long long)hftw::kPairKG * (kPairKPT - 2);
     c->pair_ok = true;
     return HFTW_OK;
 }
 
 int resolved_kernel(const hftw_ctx* c) {
     if (c->kernel_req == HFTW_KERNEL_AUTO)
-        return c->pair_ok && c->pair_auto ? HFTW_KERNEL_FUSED_PAIR
+        return c->pair_ok && c->pair_auto && c->pair_fast ? HFTW_KERNEL_FUSED_PAIR
                           : c->tma_ok ? HFTW_KERNEL_FUSED_TMA : HFTW_KERNEL_FUSED_CELL;
     return c->kernel_req;
 }
