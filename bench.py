@@ -311,16 +311,10 @@ def run_ours(args):
         # with CUDA events around every launch: hftw_set_timing)
         ctx.set_timing(True)
         ctx.step(K)
-        done = 0
         for kind, name in ((2, "multi_step"), (1, "pair"), (0, "single_step")):
-            ms, n = ctx.timing(kind)
+            ms, n, st = ctx.timing(kind)
             if n:
-                # a multi-step launch covers the steps the other kinds did not
-                spl = {0: 1, 1: 2}.get(kind)
-                kinds[name] = {"launches": n, "avg_launch_ms": ms / n, "steps_per_launch": spl}
-                done += (spl or 0) * n
-        if "multi_step" in kinds:
-            kinds["multi_step"]["steps_per_launch"] = (K - done) / kinds["multi_step"]["launches"]
+                kinds[name] = {"launches": n, "avg_launch_ms": ms / n, "steps_per_launch": st / n}
         for name, kd in kinds.items():
             # 16 B per stored cell + 16 B per column PER STEP, times the
             # steps one launch processes.  A pair pass keeps its intermediate step on

@@ -148,10 +148,12 @@ int hftw_get_kernel(const hftw_ctx* ctx);
 /* Measurement hook: when on, every step launch is bracketed by CUDA events on
  * the context stream.  hftw_get_timing returns the summed device time (ms)
  * and the number of launches of one launch kind since timing was switched
- * on: kind 0 = single-step kernels, 1 = two-step (pair) kernels, 2 = multi-step
- * (wavefront) launches of the single-step kernel's tiling. */
+ * on: kind 0 = single-step kernels, 1 = two-step (pair) passes (one launch per
+ * pass), 2 = multi-step (wavefront) launches of the single-step kernel's
+ * tiling. */
 int hftw_set_timing(hftw_ctx* ctx, int on);
-int hftw_get_timing(hftw_ctx* ctx, int kind, double* ms, int64_t* launches);
+/* steps (may be NULL): the timesteps those launches computed. */
+int hftw_get_timing(hftw_ctx* ctx, int kind, double* ms, int64_t* launches, int64_t* steps);
 
 /* Phase 1 alone (weather.cpp:118-128): in-place column physics on ENERGY.
  * mode 0 = one column per thread with the k loop in registers (the

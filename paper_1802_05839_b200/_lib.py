@@ -76,7 +76,8 @@ SIGNATURES = [
     ("hftw_step_host", C.c_int, [_P, _D, _D, _D, _D, _D]),
     ("hftw_sync", C.c_int, [_P]),
     ("hftw_set_timing", C.c_int, [_P, C.c_int]),
-    ("hftw_get_timing", C.c_int, [_P, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int64)]),
+    ("hftw_get_timing", C.c_int, [_P, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int64),
+                                  C.POINTER(C.c_int64)]),
     ("hftw_last_error", C.c_char_p, [_P]),
     ("hftw_run_reference", C.c_int, [C.POINTER(hftw_grid), C.c_int64, C.c_int, _D, _D, _D, _D]),
     ("hftw_set_stream", C.c_int, [_P, _P]),

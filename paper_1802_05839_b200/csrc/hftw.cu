@@ -135,7 +135,12 @@ struct hftw_ctx {
 
     // measurement hook (hftw_set_timing)
     bool timing = false;
-    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> tev;
+    struct TimedLaunch {
+        int kind;
+        cudaEvent_t a, b;
+        int64_t steps;
+    };
+    std::vector<TimedLaunch> tev;
 
     // decomposed run
     unsigned long long* flags = nullptr; // [4] step flags written by the neighbours
@@ -530,17 +535,19 @@ int resolved_kernel(const hftw_ctx* c) {
     return c->kernel_req;
 }
 
-// Measurement hook: events around one launch (kind 0 = single step, 1 = pair).
-int timing_mark(hftw_ctx* c, int kind, bool begin) {
+// Measurement hook: events around one launch (kind 0 = single step, 1 = pair
+// pass, 2 = multi-step) and the steps it covers.
+int timing_mark(hftw_ctx* c, int kind, bool begin, int64_t steps = 1) {
     if (!c->timing) return HFTW_OK;
     if (begin) {
         cudaEvent_t a, b;
         CUDA_TRY(c, cudaEventCreate(&a));
         CUDA_TRY(c, cudaEventCreate(&b));
-        c->tev.push_back({kind, {a, b}});
+        c->tev.push_back({kind, a, b, steps});
         CUDA_TRY(c, cudaEventRecord(a, c->stream));
     } else {
-        CUDA_TRY(c, cudaEventRecord(c->tev.back().second.second, c->stream));
+        c->tev.back().steps = steps;
+        CUDA_TRY(c, cudaEventRecord(c->tev.back().b, c->stream));
     }
     return HFTW_OK;
 }
@@ -569,7 +576,7 @@ int launch_pair(hftw_ctx* c, int src) {
         c->tm_e2[src], c->tm_sfpb, c->tm_ef[src], c->tm_sfpbf, e3(c, src), e3(c, src ^ 1), sf2(c),
         pb2(c), d, a);
     CUDA_TRY(c, cudaGetLastError());
-    return timing_mark(c, 1, false);
+    return timing_mark(c, 1, false, 2);
 }
 
 // K steps per launch with the TMA kernel's tiling (weather_wave.cuh): single
@@ -630,7 +637,7 @@ int launch_wave(hftw_ctx* c, int src, int64_t nsteps) {
     hftw::step_wave_kernel<64, kNCW><<<c->wave_ctas, (kNCW + 1) * 32, c->smem, c->stream>>>(
         c->tm_e[src], c->tm_e[src ^ 1], c->tm_sf, c->tm_pb, sf2(c), pb2(c), d, a);
     CUDA_TRY(c, cudaGetLastError());
-    return timing_mark(c, 2, false);
+    return timing_mark(c, 2, false, nsteps);
 }
 
 
@@ -1063,8 +1070,8 @@ void hftw_destroy(hftw_ctx* c) {
     if (c->gcol) cudaFree(c->gcol);
     if (c->grow) cudaFree(c->grow);
     for (auto& t : c->tev) {
-        cudaEventDestroy(t.second.first);
-        cudaEventDestroy(t.second.second);
+        cudaEventDestroy(t.a);
+        cudaEventDestroy(t.b);
     }
     if (c->flags) cudaFree(c->flags);
     if (c->done) cudaFree(c->done);
@@ -1233,30 +1240,32 @@ int hftw_set_timing(hftw_ctx* c, int on) {
     if (rc) return rc;
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     for (auto& t : c->tev) {
-        cudaEventDestroy(t.second.first);
-        cudaEventDestroy(t.second.second);
+        cudaEventDestroy(t.a);
+        cudaEventDestroy(t.b);
     }
     c->tev.clear();
     c->timing = on != 0;
     return HFTW_OK;
 }
 
-int hftw_get_timing(hftw_ctx* c, int kind, double* ms, int64_t* launches) {
+int hftw_get_timing(hftw_ctx* c, int kind, double* ms, int64_t* launches, int64_t* steps) {
     int rc = check_ctx(c);
     if (rc) return rc;
     if (!ms || !launches) return fail(c, HFTW_EINVAL, "null output");
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     double tot = 0.0;
-    int64_t n = 0;
+    int64_t n = 0, st = 0;
     for (auto& t : c->tev) {
-        if (t.first != kind) continue;
+        if (t.kind != kind) continue;
         float x = 0.f;
-        CUDA_TRY(c, cudaEventElapsedTime(&x, t.second.first, t.second.second));
+        CUDA_TRY(c, cudaEventElapsedTime(&x, t.a, t.b));
         tot += x;
         ++n;
+        st += t.steps;
     }
     *ms = tot;
     *launches = n;
+    if (steps) *steps = st;
     return HFTW_OK;
 }
 

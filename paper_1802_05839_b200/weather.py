@@ -269,12 +269,13 @@ class Context:
         """Measurement hook: CUDA events around every step launch (hftw_set_timing)."""
         self._chk(lib().hftw_set_timing(self._h, 1 if on else 0))
 
-    def timing(self, kind: int) -> Tuple[float, int]:
-        """(summed device ms, launches) of one launch kind since set_timing(True):
-        0 = single-step kernels, 1 = two-step (pair) kernels."""
-        ms, n = C.c_double(), C.c_int64()
-        self._chk(lib().hftw_get_timing(self._h, kind, C.byref(ms), C.byref(n)))
-        return ms.value, n.value
+    def timing(self, kind: int) -> Tuple[float, int, int]:
+        """(summed device ms, launches, steps) of one launch kind since
+        set_timing(True): 0 = single-step kernels, 1 = two-step (pair) passes,
+        2 = multi-step launches."""
+        ms, n, st = C.c_double(), C.c_int64(), C.c_int64()
+        self._chk(lib().hftw_get_timing(self._h, kind, C.byref(ms), C.byref(n), C.byref(st)))
+        return ms.value, n.value, st.value
 
     def physics(self, mode: int = 0) -> None:
         self._chk(lib().hftw_physics(self._h, mode))

@@ -316,7 +316,7 @@ def test_multi_step_launch_vs_oracle(coracle, shape, steps):
         ctx.set_timing(True)
         ctx.step(steps)
         ctx.step(steps)
-        ms, n = ctx.timing(2)
-        assert n == 2  # both calls were single multi-step launches
+        ms, n, st = ctx.timing(2)
+        assert n == 2 and st == 2 * steps  # both calls were single multi-step launches
         got = {f: ctx.download(f) for f in ("energy", "energy_u", "energy_surf", "energy_pbl")}
     assert_same(got, want, f"{shape}/wave/{steps}")

@@ -18,12 +18,11 @@ for kernel, n in (("fused_tma", 60), ("fused_pair", 121)):
         ctx.step(n)
         ctx.sync()
         wall = time.perf_counter() - t0
-        for kind in (0, 1):
-            ms, cnt = C.c_double(), C.c_int64()
-            lib().hftw_get_timing(ctx._h, kind, C.byref(ms), C.byref(cnt))
-            if cnt.value:
-                per = ms.value / cnt.value
-                print(f"{kernel}: kind {kind}: {cnt.value} launches, {per:.4f} ms/launch, "
-                      f"{stored / (per * 1e-3) / 1e9:.0f} GB/s algorithmic per launch")
+        for kind in (0, 1, 2):
+            ms, cnt, st = ctx.timing(kind)
+            if cnt:
+                per = ms / st  # per step
+                print(f"{kernel}: kind {kind}: {cnt} launches, {st} steps, {per:.4f} ms/step, "
+                      f"{stored / (per * 1e-3) / 1e9:.0f} GB/s algorithmic (16 B/cell-step)")
         print(f"{kernel}: {n} steps wall {wall * 1e3:.2f} ms -> {wall / n * 1e3:.4f} ms/step, "
               f"{alg * n / wall:.3e} cells/s")
