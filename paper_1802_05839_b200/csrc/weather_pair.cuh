@@ -9,21 +9,24 @@
 // (explicitly rounded IEEE ops, the reference's association order), so the
 // result is bitwise identical to two reference steps.
 //
-// Tiling (IJK store, one persistent 512-thread CTA per SM, dynamic j-major
-// work units of 62-column strips x `chunk` rows):
-//   * per row j, ONE TMA box of e_s covers columns i0-2 .. i0+63 and all k,
+// Tiling (IJK store, two persistent 256-thread CTAs per SM, dynamic j-major
+// work units of 30-column strips x 16 rows, the last ~1.5 waves of units 8 rows):
+//   * per row j, ONE TMA box of e_s covers columns i0-2 .. i0+31 and all k,
 //     one box the sf and pb rows, and -- for the two edge strips -- a 2-wide
 //     box holds the cyclic partner column of the i-ghost cell (column nx for
 //     strip 0, column 1 for the last strip).  Thread 0 refills the ring slot
-//     a row frees right after the row's barrier (no producer warp);
-//   * row jr of the intermediate P' = physics(e_{s+1}) is computed for the 64
-//     columns i0-1 .. i0+62 from slabs jr-1, jr, jr+1: 8 k-groups of <= 8
-//     planes x 64 columns = 16 warps, each thread walking its planes with a
-//     register window.  P' goes to a shared row buffer, and each thread keeps
-//     its column's last three intermediate rows in registers (a j window);
-//   * row j = jr-1 of e_{s+2} is then computed for the 62 columns i0 .. i0+61
-//     from the row buffer (i and k neighbours) and the register window (j
-//     neighbours) and stored straight to HBM.
+//     a row frees right after the row's first barrier (no producer warp);
+//   * row jr of the intermediate P' = physics(e_{s+1}) is computed for the 32
+//     columns i0-1 .. i0+30 from slabs jr-1, jr, jr+1: 8 k-groups of 7-8
+//     planes x 32 columns = 8 warps, each thread walking its planes with a
+//     register window (k).  P' goes to one of three shared row buffers;
+//   * after a barrier, row j = jr-1 of e_{s+2} is computed for the 30 columns
+//     i0 .. i0+29: the i and j-1 neighbours from the row buffers, the centre,
+//     its k neighbours and the j+1 neighbour from this thread's registers --
+//     and stored straight to HBM.  A second barrier frees the oldest buffer.
+//   * the edge planes k = 1 and nz (physics corrections, k-plane formulas)
+//     are peeled at compile time per k-group "shape", so the common planes
+//     run without them.
 // Ghost cells of e_{s+2} need intermediates from the opposite edge of the
 // domain (the reference's cyclic rules, weather.cpp:152-168).  Units on the
 // domain rim publish their ghost-adjacent intermediates (columns 0, 1, nx,
@@ -274,75 +277,6 @@ __device__ __forceinline__ void inter_ghost(const IRow& r, double* out, double* 
     }
 }
 
-// Row j of e_{s+2} for one inner column: i and k neighbours from the row
-// buffer B (row j), j neighbours and the centre from the register window
-// (P0 = row j-1, P1 = row j, P2 = row j+1).  weather.cpp:130-150 on P'.
-// NK planes from kl; FIRST / LAST as for inter_inner (compile time).
-template <int KP, int NK, bool FIRST, bool LAST>
-__device__ __forceinline__ void final_row(const double* P0, const double* P1, const double* P2,
-                                          const double* B, double* q, long long sk, int kl,
-                                          const Dom& d) {
-    const double dv = d.dv, c6 = d.c6, c5 = d.c5;
-    const double* Bk = B + (kl - 1) * kPairIC;
-#pragma unroll
-    for (int kk = 0; kk < NK; ++kk) {
-        double s = dadd(Bk[kk * kPairIC - 1], Bk[kk * kPairIC + 1]);
-        s = dadd(s, P0[kk]);
-        s = dadd(s, P2[kk]);
-        double v;
-        if (FIRST && kk == 0) {
-            const double kp = kk + 1 < NK ? P1[kk + 1] : Bk[(kk + 1) * kPairIC];
-            v = dadd(dmul(c5, P1[kk]), dmul(dv, dadd(s, kp)));
-        } else if (LAST && kk == NK - 1) {
-            const double km = kk > 0 ? P1[kk - 1] : Bk[(kk - 1) * kPairIC];
-            v = dadd(dmul(c5, P1[kk]), dmul(dv, dadd(s, km)));
-        } else {
-            const double km = kk > 0 ? P1[kk - 1] : Bk[(kk - 1) * kPairIC];
-            const double kp = kk + 1 < NK ? P1[kk + 1] : Bk[(kk + 1) * kPairIC];
-            v = dadd(dmul(c6, P1[kk]), dmul(dv, dadd(dadd(s, km), kp)));
-        }
-        *q = v;
-        q += sk;
-    }
-}
-
-// One row of the fast shapes in ONE straight-line block: the final row j =
-// jr-1 (from the row buffer B of row j and the register window) and the
-// intermediate row jr (from the slabs).  The final's first partial sums
-// ((W + E) + S, weather.cpp:134-136 order) need nothing from row jr, so the
-// compiler can interleave them with the intermediate's chains; the
-// intermediate's row-buffer stores come last so no shared load has to wait
-// behind them.  The final value is stored only when `store` (the first two
-// rows of a unit have no final row; edge lanes have no output column).
-template <int KP, int NK, bool FIRST, bool LAST>
-__device__ __forceinline__ void row_fast(const IRow& r, double* P0, double* P1, double* P2,
-                                         double* ibrow, const double* B, double* q, long long sk,
-                                         int kl, bool store, const Dom& d) {
-    const double dv = d.dv, c6 = d.c6, c5 = d.c5;
-    const double* Bk = B + (kl - 1) * kPairIC;
-    double ps[NK], bm = 0.0, bp = 0.0;
-#pragma unroll
-    for (int kk = 0; kk < NK; ++kk)
-        ps[kk] = dadd(dadd(Bk[kk * kPairIC - 1], Bk[kk * kPairIC + 1]), P0[kk]);
-    if (!FIRST) bm = Bk[-kPairIC];        // P'(k = kl-1) of row j
-    if (!LAST) bp = Bk[NK * kPairIC];     // P'(k = kh+1) of row j
-    inter_inner<KP, NK, FIRST, LAST>(r, P2, nullptr, kl, d);
-#pragma unroll
-    for (int kk = 0; kk < NK; ++kk) {
-        const double s = dadd(ps[kk], P2[kk]);
-        const double km = kk > 0 ? P1[kk - 1] : bm;
-        const double kp = kk + 1 < NK ? P1[kk + 1] : bp;
-        double v;
-        if (FIRST && kk == 0) v = dadd(dmul(c5, P1[kk]), dmul(dv, dadd(s, kp)));
-        else if (LAST && kk == NK - 1) v = dadd(dmul(c5, P1[kk]), dmul(dv, dadd(s, km)));
-        else v = dadd(dmul(c6, P1[kk]), dmul(dv, dadd(dadd(s, km), kp)));
-        if (store) q[(long long)kk * sk] = v;
-    }
-    double* qi = ibrow + (kl - 1) * kPairIC;
-#pragma unroll
-    for (int kk = 0; kk < NK; ++kk) qi[kk * kPairIC] = P2[kk];
-}
-
 // Row j of e_{s+2}: the i neighbours from the row buffer of row j (B0), the
 // j-1 neighbour from the buffer of row j-1 (Bm), and the centre, its k
 // neighbours and the j+1 neighbour from registers (Pc = row j, Pn = row j+1,
@@ -393,36 +327,6 @@ __device__ __forceinline__ void final_smem_generic(const double* Bm, const doubl
         if (k == 1) v = dadd(dmul(d.c5, B0[o]), dmul(dv, dadd(s, B0[o + kPairIC])));
         else if (k == nz) v = dadd(dmul(d.c5, B0[o]), dmul(dv, dadd(s, B0[o - kPairIC])));
         else v = dadd(dmul(d.c6, B0[o]), dmul(dv, dadd(dadd(s, B0[o - kPairIC]), B0[o + kPairIC])));
-        q[(long long)kk * sk] = v;
-    }
-}
-
-template <int KP>
-__device__ __forceinline__ void final_generic(const double* P0, const double* P1, const double* P2,
-                                           const double* B, double* q, long long sk, int kl,
-                                           int nk, const Dom& d) {
-    const int nz = d.nz;
-    const double dv = d.dv;
-#pragma unroll
-    for (int kk = 0; kk < KP; ++kk) {
-        if (kk >= nk) break;
-        const int k = kl + kk;
-        const int o = (k - 1) * kPairIC;
-        double s = dadd(B[o - 1], B[o + 1]);
-        s = dadd(s, P0[kk]);
-        s = dadd(s, P2[kk]);
-        double v;
-        if (k == 1) {
-            const double kp = kk + 1 < nk ? P1[kk + 1] : B[o + kPairIC];
-            v = dadd(dmul(d.c5, P1[kk]), dmul(dv, dadd(s, kp)));
-        } else if (k == nz) {
-            const double km = kk > 0 ? P1[kk - 1] : B[o - kPairIC];
-            v = dadd(dmul(d.c5, P1[kk]), dmul(dv, dadd(s, km)));
-        } else {
-            const double km = kk > 0 ? P1[kk - 1] : B[o - kPairIC];
-            const double kp = kk + 1 < nk ? P1[kk + 1] : B[o + kPairIC];
-            v = dadd(dmul(d.c6, P1[kk]), dmul(dv, dadd(dadd(s, km), kp)));
-        }
         q[(long long)kk * sk] = v;
     }
 }
@@ -559,7 +463,7 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
     extern __shared__ __align__(128) unsigned char smem[];
     const PairGeom G = pair_geom(d.nz);
     const int NS = a.ns;
-    // intermediate row buffer of row j: ib0 + (j & 1) * ibn
+    // intermediate row buffers: ib0 + b * ibn, b rotating over kPairNIB
     double* const ib0 = reinterpret_cast<double*>(smem + (size_t)NS * G.stage);
     const int ibn = G.ib / 8;
     uint64_t* full =
