@@ -279,7 +279,7 @@ __global__ void exchange_kernel(const double* __restrict__ e, const double* __re
 //      storage-order penalty).  Loads are batched 8 deep.
 //  physics_rows_kernel (IJK): one (j,k) row per block pass, i across threads.
 //  physics_kij_kernel (KIJ): one column per warp, lanes along k -- the
-//      KIJ-aware mapping.
+//      KIJ-aware mapping; physics_kij_stream_kernel streams whole rows.
 //------------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) physics_column_kernel(double* __restrict__ e,
                                                              const double* __restrict__ sf,
@@ -324,6 +324,59 @@ __global__ void __launch_bounds__(256) physics_rows_kernel(double* __restrict__ 
             if (k == 1) sfv = __ldg(srow + i);
             if (k == d.nz) pbv = __ldg(brow + i);
             row[i] = phys<true>(row[i], k, d.nz, sfv, pbv, d.ri, d.tv);
+        }
+    }
+}
+
+// KIJ, streaming: consecutive columns of a row are ONE contiguous run of
+// Pk-double columns, so a warp takes 16 columns at a time and its lanes walk
+// that run 32 doubles apart -- fully coalesced -- tracking (column, k)
+// incrementally (no divisions; Pk >= 32 assumed, else the warp kernel runs).
+__global__ void __launch_bounds__(256) physics_kij_stream_kernel(double* __restrict__ e,
+                                                                 const double* __restrict__ sf,
+                                                                 const double* __restrict__ pb,
+                                                                 Dom d, int pk) {
+    constexpr int CPW = 16; // columns per warp task
+    const Owned o = owned(d);
+    const int ni = o.i1 - o.i0 + 1, nj = o.j1 - o.j0 + 1;
+    const int tasks_row = (ni + CPW - 1) / CPW;
+    const long long tasks = (long long)tasks_row * nj;
+    const int lane = threadIdx.x & 31;
+    const long long warps = (long long)gridDim.x * (blockDim.x >> 5);
+    for (long long w = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); w < tasks;
+         w += warps) {
+        const int j = o.j0 + (int)(w / tasks_row);
+        const int c0 = o.i0 + (int)(w % tasks_row) * CPW;
+        const int nc = min(CPW, o.i1 - c0 + 1);
+        double* base = e + c0 * d.si + j * d.sj; // column c0, k = 1
+        const double* sfr = sf + j * d.s2j;
+        const double* pbr = pb + j * d.s2j;
+        int c = 0, kk = lane; // this lane's element: column c0 + c, plane kk + 1
+        const int n = nc * pk;
+        for (int q = lane; q < n; q += 4 * 32) {
+            // four loads in flight per lane before any store
+            double v[4];
+            int cs[4], ks[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                cs[u] = c;
+                ks[u] = kk;
+                v[u] = q + 32 * u < n ? base[q + 32 * u] : 0.0;
+                kk += 32;
+                if (kk >= pk) {
+                    kk -= pk;
+                    ++c;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (q + 32 * u >= n || ks[u] >= d.nz) continue;
+                const int k = ks[u] + 1, i = c0 + cs[u];
+                double sfv = 0.0, pbv = 0.0;
+                if (k == 1) sfv = __ldg(sfr + i);
+                if (k == d.nz) pbv = __ldg(pbr + i);
+                base[q + 32 * u] = phys<true>(v[u], k, d.nz, sfv, pbv, d.ri, d.tv);
+            }
         }
     }
 }

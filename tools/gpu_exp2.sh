@@ -1,4 +1,3 @@
-timeout 120 python tools/pair_small.py 100 37 58; echo small=$?
-timeout 600 python -m pytest tests/test_parity_gpu.py -x -q -k "pair or golden or random" 2>&1 | tail -1 | cut -c1-200
-echo "== pconv"; timeout 200 python tools/pair_time.py 2>&1 | grep "kind 1"
-echo "== no pconv"; HFTW_LIBRARY=$PWD/tools/exp/nopconv.so timeout 200 python tools/pair_time.py 2>&1 | grep "kind 1"
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_parity_gpu.py -x -q -k "hash or energy_u or random" > gpurun_out/t.log 2>&1; tail -1 gpurun_out/t.log
+for v in 0 1; do HFTW_KIJ_PHYS_WARP=$v timeout 200 python bench.py --workload physics --layout kij --physics-mode 1 --steps 100 --warmup 5 --no-e2e --no-cpu-baseline | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('warp=$v', d['ms_per_step'], d['roofline']['frac'])"; done
