@@ -512,6 +512,10 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
         const bool owns_i = (gi >= i0 && gi <= min(i0 + kPairTX - 1, nx + 1)) ||
                             (st == 0 && gi == 0) || (st == a.nstrips - 1 && gi == nx + 1);
         const bool ig = gi == 0 || gi == nx + 1;
+        // does this thread ever publish in this unit (a ghost-adjacent column, or
+        // an inner column whose rows 0, 1, ny, ny+1 may fall in this unit)?
+        const bool pub_col = owns_i && (gi <= 1 || gi >= nx);
+        const bool pub_row = owns_i && gi >= 1 && gi <= nx && (ja <= 2 || jb >= ny - 1);
         const int fsel = (a.fp + pair_far_col(st, a.nstrips, nx)) & 1;
         const bool do_final = cc >= 2 && cc <= kPairTX + 1 && gi <= nx && nk > 0;
         RingPos Ra = R0;          // slab jr-1
@@ -554,8 +558,10 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
                     }
                     break;
                 }
-                const bool owns_j = (jr >= ja && jr <= jb) || jr == 0 || jr == ny + 1;
-                if (owns_i && owns_j) pair_publish<KPT>(PW2, kl, nk, gi, jr, d, a);
+                if (pub_col || pub_row) {
+                    const bool owns_j = (jr >= ja && jr <= jb) || jr == 0 || jr == ny + 1;
+                    if (owns_j) pair_publish<KPT>(PW2, kl, nk, gi, jr, d, a);
+                }
             }
             __syncthreads(); // intermediate row jr complete; slab jr-1 free
             // refill slab jr-1's slot (and, after the last row, those of jb+1, jb+2)
