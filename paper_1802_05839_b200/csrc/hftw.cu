@@ -521,9 +521,9 @@ int setup_pair(hftw_ctx* c) {
     CUDA_TRY(c, cudaMemset(c->d_pair, 0, ints * sizeof(int)));
     CUDA_TRY(c, cudaMalloc(&c->gcol, (size_t)(4 * (ny + 2) * c->nz) * sizeof(double)));
     CUDA_TRY(c, cudaMalloc(&c->grow, (size_t)(4 * c->nz * (c->lnx + 2)) * sizeof(double)));
-    // the compile-time row shapes cover groups of KPT-2 .. KPT planes; other nz run
+    // the compile-time row shapes cover groups of KPT-1 .. KPT planes; other nz run
     // the generic (runtime plane checks) path, which AUTO leaves to the TMA kernel
-    c->pair_fast = c->nz >= (long long)hftw::kPairKG * (kPairKPT - 2);
+    c->pair_fast = c->nz >= (long long)hftw::kPairKG * (kPairKPT - 1);
     c->pair_ok = true;
     return HFTW_OK;
 }

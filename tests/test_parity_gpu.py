@@ -71,12 +71,12 @@ def test_golden_cases(golden, layout, kernel):
 
 @pytest.mark.parametrize("layout", LAYOUTS)
 def test_auto_kernel_selected(layout):
-    # AUTO: two-step passes (IJK, one domain, 48 <= nz <= 60: the compile-time row
+    # AUTO: two-step passes (IJK, one domain, 56 <= nz <= 60: the compile-time row
     # shapes); the TMA kernel otherwise (fused_pair still runs other nz on request)
     with W.Context(W.GridConfig(nx=100, ny=40, nz=58), layout=layout) as ctx:
         assert ctx.kernel == ("fused_pair" if layout == "ijk" else "fused_tma")
         assert ctx.launches_per_step == 1
-    with W.Context(W.GridConfig(nx=100, ny=40, nz=20), layout=layout) as ctx:
+    with W.Context(W.GridConfig(nx=100, ny=40, nz=50), layout=layout) as ctx:
         assert ctx.kernel == "fused_tma"
         if layout == "ijk":
             ctx.set_kernel("fused_pair")
