@@ -77,3 +77,29 @@ def test_dump_writer_round_trip(tmp_path, coracle):
         a = W.read_field(f, d)
     assert d.ok()
     assert np.array_equal(a.data, coracle.run_reference(O.grid_from(cfg), 10).energy)
+
+
+@pytest.mark.gpu
+def test_simulate_with_pair_passes(coracle):
+    """nz = 58: the steps between outputs run as two-step passes (+ a trailing
+    single step); every output and the final state bitwise."""
+    dt, odt, steps = 0.1, 1.0, 37
+    cfg = W.GridConfig(nx=70, ny=45, nz=58, timestep=dt, output_timestep=odt)
+    g = O.grid_from(cfg)
+    got = []
+    with W.Context(cfg) as ctx:
+        assert ctx.kernel == "fused_pair"
+        ctx.init()
+        ctx.set_timing(True)
+        nsteps, nwrites = ctx.simulate(0.0, (steps - 0.5) * dt, dt, odt,
+                                       lambda tag, t, f: got.append((t, f.copy())))
+        assert ctx.timing(1)[1] > 0  # pair passes were used between the outputs
+        final = ctx.download("energy")
+        final_u = ctx.download("energy_u")
+    sched, done = driver_schedule(steps, dt, odt)
+    assert nsteps == done and nwrites == len(sched)
+    for (t, f), (ts, n) in zip(got, sched):
+        assert t == ts
+        assert np.array_equal(f, coracle.run_reference(g, n).energy), (t, n)
+    ref = coracle.run_reference(g, steps)
+    assert np.array_equal(final, ref.energy) and np.array_equal(final_u, ref.energy_u)

@@ -320,3 +320,46 @@ def test_multi_step_launch_vs_oracle(coracle, shape, steps):
         assert n == 2 and st == 2 * steps  # both calls were single multi-step launches
         got = {f: ctx.download(f) for f in ("energy", "energy_u", "energy_surf", "energy_pbl")}
     assert_same(got, want, f"{shape}/wave/{steps}")
+
+
+@pytest.mark.parametrize("kernel,steps", [("auto", 7), ("fused_tma", 6)])
+def test_asuca_random_state_non_default_constants(coracle, kernel, steps):
+    """BASELINE's full size from a random state with non-default constants: the
+    pair passes (auto) and the multi-step launch (fused_tma), bitwise."""
+    rng = np.random.default_rng(1802)
+    cfg = W.GridConfig(nx=1581, ny=1301, nz=58, diffusion_velocity=0.1375,
+                       radiation_intensity=-0.21, transfer_velocity=0.047,
+                       surf_energy=312.5, pbl_energy=187.25)
+    g = O.grid_from(cfg)
+    n3, n2 = O.shapes(g)
+    s0 = O.State(rng.uniform(150, 350, n3), rng.uniform(150, 350, n3),
+                 rng.uniform(150, 350, n2), rng.uniform(150, 350, n2))
+    want = coracle.steps(g, s0, steps).fields()
+    got = run_device(cfg, steps, "ijk", kernel, s0.fields())
+    assert_same(got, want, f"asuca/{kernel}/{steps}")
+
+
+@pytest.mark.parametrize("shape", [(100, 37, 58), (33, 20, 37), (17, 9, 2), (40, 6, 31),
+                                   (64, 64, 33)])
+@pytest.mark.parametrize("layout", LAYOUTS)
+@pytest.mark.parametrize("mode", [0, 1])
+def test_physics_phase_vs_oracle(coracle, shape, layout, mode):
+    """Column physics alone (weather.cpp:118-128), every mapping and layout, odd
+    nz (KIJ column padding) and nz < 32 (the KIJ warp kernel): bitwise."""
+    nx, ny, nz = shape
+    rng = np.random.default_rng(nx + 100 * ny + 10000 * nz)
+    cfg = W.GridConfig(nx=nx, ny=ny, nz=nz, radiation_intensity=float(rng.uniform(-1, 1)),
+                       transfer_velocity=float(rng.uniform(0, 0.2)))
+    g = O.grid_from(cfg)
+    n3, n2 = O.shapes(g)
+    e = rng.uniform(150, 350, n3)
+    sf, pb = rng.uniform(150, 350, n2), rng.uniform(150, 350, n2)
+    want = coracle.physics(g, e, sf, pb)
+    with W.Context(cfg, layout=layout) as ctx:
+        ctx.upload("energy", np.ascontiguousarray(e))
+        ctx.upload("energy_surf", np.ascontiguousarray(sf))
+        ctx.upload("energy_pbl", np.ascontiguousarray(pb))
+        ctx.physics(mode)
+        got = ctx.download("energy")
+    bad = np.flatnonzero(got != want)
+    assert bad.size == 0, (shape, layout, mode, bad[:5])
