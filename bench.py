@@ -362,7 +362,8 @@ def run_ours(args):
         avg_launch_s = statistics.mean(launch_ms) * 1e-3
         launches = K * (ctx.launches_per_step if args.workload == "full" else 1)
     achieved = alg_bytes / avg_launch_s / 1e9
-    traffic = ncu_traffic(args.workload, args.layout, dom_name) if world == 1 else None
+    tkey = f"mode{args.physics_mode}" if args.workload == "physics" else dom_name
+    traffic = ncu_traffic(args.workload, args.layout, tkey) if world == 1 else None
     if traffic is not None and dom in ("multi_step", "pair"):
         traffic *= kinds[dom]["steps_per_launch"]  # the capture is stored per step
 
