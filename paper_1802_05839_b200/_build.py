@@ -10,8 +10,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libhftw.so")
 SOURCES = [os.path.join(CSRC, "hftw.cu")]
-DEPS = SOURCES + [os.path.join(CSRC, "weather_kernels.cuh"), os.path.join(CSRC, "weather_pair.cuh"),
-                  os.path.join(ROOT, "include", "hftw.h")]
+DEPS = SOURCES + sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cuh")) + [
+    os.path.join(ROOT, "include", "hftw.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -54,8 +54,10 @@ constexpr int kPairMinBlocks = kPairThreads <= 256 ? 2 : 1; // CTAs per SM the t
 #ifndef HFTW_PAIR_NIB
 #define HFTW_PAIR_NIB 3
 #endif
-// intermediate row buffers: 3 (rows j-1, j, j+1; two barriers per row) or 4 (one
-// barrier per row: the buffer a row overwrites was last read two rows earlier)
+// intermediate row buffers (rows j-1, j, j+1), one CTA barrier per row
+#ifndef HFTW_PAIR_BAR2
+#define HFTW_PAIR_BAR2 0 // 1: the earlier second barrier per row (A/B measurement only)
+#endif
 constexpr int kPairNIB = HFTW_PAIR_NIB;
 
 __host__ __device__ inline int round128(int b) { return (b + 127) / 128 * 128; }
@@ -588,8 +590,13 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
                 default: final_smem_generic<KPT>(Bm, B0, Bp, q, d.sk, kl, nk, d); break;
                 }
             }
-            if (kPairNIB == 3)
-                __syncthreads(); // the final row is done reading buffer ib2 (next row's target)
+            // No second barrier: the next row's target buffer (ib2) is read here only
+            // as Bm, at this thread's own column and planes; the neighbour warps'
+            // reads of it (their B0 k-boundary planes, one row earlier) are ordered
+            // before the next write by this row's barrier.
+#if HFTW_PAIR_BAR2
+            __syncthreads();
+#endif
 #pragma unroll
             for (int kk = 0; kk < KPT; ++kk) PW1[kk] = PW2[kk];
             ibi = ibi == kPairNIB - 1 ? 0 : ibi + 1;
