@@ -488,9 +488,20 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
     // thread -> (intermediate column cc = 1 .. 64 = logical i0-2+cc, k-group g)
     const int cc = 1 + (tid % kPairIC);
     const int g = tid / kPairIC;
-    // balanced k-groups: planes kl .. kh, nk = kh - kl + 1 <= KPT
-    const int kl = 1 + (g * nz) / kPairKG, kh = ((g + 1) * nz) / kPairKG;
-    const int nk = kh - kl + 1;
+    // k-groups: planes kl .. kh, nk = kh - kl + 1 <= KPT.  The first and last
+    // groups carry the surface / boundary-layer corrections of planes 1 and nz
+    // (about one extra plane of work), so the nz % KG extra planes go to the
+    // middle groups first: nz = 58 -> 7 8 8 7 7 7 7 7.
+    int kl = 1, nk = 0;
+    {
+        const int base = nz / kPairKG, rem = nz % kPairKG;
+        for (int q = 0; q <= g; ++q) {
+            kl += nk;
+            nk = base + ((q >= 1 && q <= min(rem, kPairKG - 2)) ||
+                         (rem == kPairKG - 1 && q == kPairKG - 1));
+        }
+    }
+    const int kh = kl + nk - 1;
     const bool kfirst = kl == 1, klast = kh == nz;
     // compile-time row shapes: nk in {KPT, KPT-1} x (first, last); else generic
     const int fl = (kfirst ? 1 : 0) + (klast ? 2 : 0);
