@@ -505,8 +505,10 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
     const bool kfirst = kl == 1, klast = kh == nz;
     // compile-time row shapes: nk in {KPT, KPT-1} x (first, last); else generic
     const int fl = (kfirst ? 1 : 0) + (klast ? 2 : 0);
+    // (an edge group of KPT planes occurs only for nz > 62, beyond the pair
+    // kernel's 2-CTA shared-memory budget: it takes the generic path)
     int shape = nz < 2 * kPairKG || fl == 3 ? 16
-                : nk == KPT ? fl : nk == KPT - 1 ? 4 + fl : nk == KPT - 2 ? 8 + fl : 16;
+                : nk == KPT ? (fl ? 16 : 0) : nk == KPT - 1 ? 4 + fl : 16;
 
     double PW2[KPT]; // this row's intermediate values
     double PW1[KPT]; // the previous row's (the final row's centre)
@@ -554,8 +556,6 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
                 const bool ghost = ig || jr == 0 || jr == ny + 1;
                 switch (ghost ? 16 : shape) {
                 case 0: inter_inner<KPT, KPT, false, false>(r, PW2, ibrow, kl, d); break;
-                case 1: inter_inner<KPT, KPT, true, false>(r, PW2, ibrow, kl, d); break;
-                case 2: inter_inner<KPT, KPT, false, true>(r, PW2, ibrow, kl, d); break;
                 case 4: inter_inner<KPT, KPT - 1, false, false>(r, PW2, ibrow, kl, d); break;
                 case 5: inter_inner<KPT, KPT - 1, true, false>(r, PW2, ibrow, kl, d); break;
                 case 6: inter_inner<KPT, KPT - 1, false, true>(r, PW2, ibrow, kl, d); break;
@@ -593,8 +593,6 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
                             (long long)(kl - 1) * d.sk;
                 switch (shape) {
                 case 0: final_smem<KPT, false, false>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d); break;
-                case 1: final_smem<KPT, true, false>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d); break;
-                case 2: final_smem<KPT, false, true>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d); break;
                 case 4: final_smem<KPT - 1, false, false>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d); break;
                 case 5: final_smem<KPT - 1, true, false>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d); break;
                 case 6: final_smem<KPT - 1, false, true>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d); break;

@@ -71,7 +71,7 @@ def test_golden_cases(golden, layout, kernel):
 
 @pytest.mark.parametrize("layout", LAYOUTS)
 def test_auto_kernel_selected(layout):
-    # AUTO: two-step passes (IJK, one domain, 56 <= nz <= 60: the compile-time row
+    # AUTO: two-step passes (IJK, one domain, 56 <= nz <= 58: the compile-time row
     # shapes); the TMA kernel otherwise (fused_pair still runs other nz on request)
     with W.Context(W.GridConfig(nx=100, ny=40, nz=58), layout=layout) as ctx:
         assert ctx.kernel == ("fused_pair" if layout == "ijk" else "fused_tma")
@@ -243,7 +243,10 @@ def test_step_host_after_device_steps(coracle):
 
 
 @pytest.mark.parametrize("shape", [(100, 37, 58), (64, 64, 2), (65, 3, 9), (2, 2, 2), (33, 200, 17),
-                                   (129, 2, 64), (128, 70, 58), (191, 97, 31), (1, 1, 1)])
+                                   (129, 2, 64), (128, 70, 58), (191, 97, 31), (1, 1, 1),
+                                   # every k-group split with compile-time row shapes
+                                   # (nz 56-58), and the first nz past the smem budget
+                                   (70, 45, 56), (61, 33, 57), (95, 20, 59)])
 @pytest.mark.parametrize("steps", [3, 4, 5, 8])
 def test_pair_kernel_vs_oracle(coracle, shape, steps):
     """Two steps per pass (intermediate field on chip): bitwise against the oracle on
@@ -261,9 +264,10 @@ def test_pair_kernel_vs_oracle(coracle, shape, steps):
     s0 = O.State(rng.uniform(150, 350, n3), rng.uniform(150, 350, n3),
                  rng.uniform(150, 350, n2), rng.uniform(150, 350, n2))
     want = coracle.steps(g, s0, steps).fields()
-    if nz > 60:
-        # three intermediate row buffers + a 4-deep slab ring exceed shared memory:
-        # the pair kernel is refused and AUTO falls back to the single-step kernel
+    if nz > 58:
+        # three intermediate row buffers + a 4-deep slab ring for two CTAs per SM
+        # exceed shared memory: the pair kernel is refused and AUTO falls back to
+        # the single-step kernel
         assert not available(cfg, "ijk", "fused_pair")
         got = run_device(cfg, steps, "ijk", "auto", s0.fields())
     else:
