@@ -536,6 +536,14 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
         RingPos Ra = R0;          // slab jr-1
         RingPos Rb = Ra.next(NS); // slab jr
         RingPos Rc = Rb.next(NS); // slab jr+1
+        // the three slabs at this thread's column, rotated with the ring
+        const unsigned char* sm_ = smem + (size_t)Ra.slot * G.stage + cc * 8;
+        const unsigned char* s0_ = smem + (size_t)Rb.slot * G.stage + cc * 8;
+        const unsigned char* sp_ = smem + (size_t)Rc.slot * G.stage + cc * 8;
+        // this thread's output column at row ja-2 (the final row of jr = ja-1),
+        // advanced one row per iteration
+        double* qrow = u + (long long)gi * d.si + (long long)(ja - 2) * d.sj +
+                       (long long)(kl - 1) * d.sk;
         mbar_wait(&full[Rb.slot], Rb.par);
         for (int jr = ja - 1; jr <= jb + 1; ++jr) {
             mbar_wait(&full[Rc.slot], Rc.par);
@@ -544,15 +552,12 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
             const int ib2 = ib1 == 0 ? kPairNIB - 1 : ib1 - 1;
             double* ibrow = ib0 + ibi * ibn + (cc - 1);
             if (indom) {
-                const unsigned char* sm_ = smem + (size_t)Ra.slot * G.stage;
-                const unsigned char* s0_ = smem + (size_t)Rb.slot * G.stage;
-                const unsigned char* sp_ = smem + (size_t)Rc.slot * G.stage;
-                const IRow r{reinterpret_cast<const double*>(sm_) + cc,
-                             reinterpret_cast<const double*>(s0_) + cc,
-                             reinterpret_cast<const double*>(sp_) + cc,
-                             reinterpret_cast<const double*>(sm_ + G.slab) + cc,
-                             reinterpret_cast<const double*>(s0_ + G.slab) + cc,
-                             reinterpret_cast<const double*>(sp_ + G.slab) + cc};
+                const IRow r{reinterpret_cast<const double*>(sm_),
+                             reinterpret_cast<const double*>(s0_),
+                             reinterpret_cast<const double*>(sp_),
+                             reinterpret_cast<const double*>(sm_ + G.slab),
+                             reinterpret_cast<const double*>(s0_ + G.slab),
+                             reinterpret_cast<const double*>(sp_ + G.slab)};
                 const bool ghost = ig || jr == 0 || jr == ny + 1;
                 switch (ghost ? 16 : shape) {
                 case 0: inter_inner<KPT, KPT, false, false>(r, PW2, ibrow, kl, d); break;
@@ -561,9 +566,10 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
                 case 6: inter_inner<KPT, KPT - 1, false, true>(r, PW2, ibrow, kl, d); break;
                 default:
                     if (ghost) {
-                        const double* fb = reinterpret_cast<const double*>(s0_ + G.slab + G.sfpb);
+                        const unsigned char* sb = s0_ - cc * 8;
+                        const double* fb = reinterpret_cast<const double*>(sb + G.slab + G.sfpb);
                         const double* fsp =
-                            reinterpret_cast<const double*>(s0_ + G.slab + G.sfpb + G.fcol);
+                            reinterpret_cast<const double*>(sb + G.slab + G.sfpb + G.fcol);
                         inter_ghost<KPT>(r, PW2, ibrow, kl, nk, gi, jr, cc, i0, d, e, sf, pb, fb,
                                          fsp, fsel);
                     } else {
@@ -589,8 +595,7 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
                 const double* Bm = ib0 + ib2 * ibn + (cc - 1);
                 const double* B0 = ib0 + ib1 * ibn + (cc - 1);
                 const double* Bp = ib0 + ibi * ibn + (cc - 1);
-                double* q = u + (long long)gi * d.si + (long long)(jr - 1) * d.sj +
-                            (long long)(kl - 1) * d.sk;
+                double* q = qrow;
                 switch (shape) {
                 case 0: final_smem<KPT, false, false>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d); break;
                 case 4: final_smem<KPT - 1, false, false>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d); break;
@@ -612,6 +617,10 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
             Ra = Rb;
             Rb = Rc;
             Rc = Rc.next(NS);
+            sm_ = s0_;
+            s0_ = sp_;
+            sp_ = smem + (size_t)Rc.slot * G.stage + cc * 8;
+            qrow += d.sj;
         }
         R0 = Rc; // slabs jb+1, jb+2 were Ra, Rb: the next unit starts after them
         // rim units: count the ghost producers; the second one computes the ghosts
