@@ -291,10 +291,16 @@ def run_ours(args):
                 evs[0][0].record(stream)
                 ctx.step(K)
                 evs[0][1].record(stream)
+            elif flush is None:
+                # back-to-back calls, one event pair around all K (per-call events
+                # would add their own gaps); per-launch times come from a second pass
+                evs[0][0].record(stream)
+                for i in range(K):
+                    one()
+                evs[-1][1].record(stream)
             else:
                 for i in range(K):
-                    if flush is not None:
-                        flush()  # on `stream`: outside the per-launch events
+                    flush()  # on `stream`: outside the per-launch events
                     evs[i][0].record(stream)
                     one()
                     evs[i][1].record(stream)
@@ -302,8 +308,19 @@ def run_ours(args):
         t_wall = time.perf_counter() - t_wall
     torch.cuda.synchronize()
     barrier()
+    if flush is None:
+        total_ms = evs[0][0].elapsed_time(evs[-1][1])
+    if not whole and flush is None:
+        # diagnostic pass: the same K calls with events around each (kernel durations)
+        with torch.cuda.stream(stream):
+            for i in range(K):
+                evs[i][0].record(stream)
+                one()
+                evs[i][1].record(stream)
+        stream.synchronize()
     launch_ms = [a.elapsed_time(b) for a, b in evs]
-    total_ms = evs[0][0].elapsed_time(evs[-1][1]) if flush is None else sum(launch_ms)
+    if flush is not None:
+        total_ms = sum(launch_ms)
     clocks = sampler.summary()
     kinds = {}
     if whole:

@@ -142,6 +142,25 @@ def test_diffusion_only_hash(golden, coracle):
             assert coracle.fnv(ctx.download("energy")) == d["fnv1a64"]["u"], layout
 
 
+@pytest.mark.parametrize("shape", [(256, 256, 64), (37, 20, 17), (2, 2, 2), (70, 9, 33)])
+def test_diffusion_sweep_vs_oracle(coracle, shape):
+    """A diffusion-only sweep (weather.cpp:130-168 on the post-physics field) of a
+    random state: bitwise."""
+    nx, ny, nz = shape
+    rng = np.random.default_rng(nx + 7 * ny + 31 * nz)
+    cfg = W.GridConfig(nx=nx, ny=ny, nz=nz, diffusion_velocity=float(rng.uniform(0, 1 / 6)))
+    g = O.grid_from(cfg)
+    n3, n2 = O.shapes(g)
+    e = rng.uniform(150, 350, n3)
+    want = coracle.diffuse(g, e.copy())
+    with W.Context(cfg) as ctx:
+        ctx.upload("energy", e)
+        ctx.diffuse()
+        got = ctx.download("energy")
+    bad = np.flatnonzero(got.view(np.uint64) != want.view(np.uint64))
+    assert bad.size == 0, (shape, bad[:5])
+
+
 def test_energy_u_observability(coracle):
     """energy_u after a step is the post-physics, pre-diffusion field
     (weather.cpp:118-128 in place, then the swap at :170)."""
