@@ -131,6 +131,7 @@ struct hftw_ctx {
     // multi-step wavefront launch (weather_wave.cuh): single-domain IJK
     bool wave_ok = false;
     int wave_chunk = 0, wave_nchunks = 0, wave_ctas = 0, wave_gtasks = 0;
+    bool wave_pref = false;     // multi-step launch preferred over one launch per step
     int* d_wave = nullptr;      // sched[2] + chunk_done[nchunks] + ghost_done[1]
 
     // measurement hook (hftw_set_timing)
@@ -616,6 +617,16 @@ int setup_wave(hftw_ctx* c) {
     }
     chunk = std::min<long long>(ny, chunk);
     c->wave_chunk = (int)chunk;
+    // Prefer it over one launch per step only where a step is short: at ASUCA size
+    // (6.9 units of 32 rows per CTA) separate launches run 0.383 ms/step against
+    // 0.397 (less DRAM traffic: 1.05x vs 1.10x), while for the 1/4 and 1/8 ranks of a
+    // 2x2 / 2x4 decomposition (1.8 and 1.0 units per CTA) the multi-step launch is
+    // 3% and 12% faster (tools/gpu_exp10.sh).  HFTW_WAVE=1 forces it (tests).
+    {
+        const long long slots = (long long)per_sm * c->num_sms;
+        const long long units32 = (long long)c->nstrips * ((ny + 31) / 32);
+        c->wave_pref = env_int("HFTW_WAVE", 0) != 0 || units32 * 10 < slots * 27;
+    }
     c->wave_nchunks = (int)((ny + chunk - 1) / chunk);
     c->wave_gtasks = std::max(1, std::min(16, (int)((c->lnx + 2) * c->nz / 2048)));
     const long long units = (long long)c->nstrips * c->wave_nchunks + c->wave_gtasks;
@@ -1225,7 +1236,7 @@ int hftw_step(hftw_ctx* c, int64_t nsteps) {
         nsteps -= 2 * pairs;
     }
     if ((k == HFTW_KERNEL_FUSED_TMA || k == HFTW_KERNEL_FUSED_PAIR) && c->wave_ok &&
-        nsteps >= 2 && c->tma_ok) {
+        c->wave_pref && nsteps >= 2 && c->tma_ok) {
         // all steps in one persistent launch (weather_wave.cuh); chunks of
         // at most 2^20 steps keep the work-list index in an int (decomposed:
         // kMaxWaveStepsDist, the per-step completion counters)

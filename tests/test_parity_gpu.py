@@ -345,10 +345,13 @@ def test_multi_step_launch_vs_oracle(coracle, shape, steps):
     assert_same(got, want, f"{shape}/wave/{steps}")
 
 
-@pytest.mark.parametrize("kernel,steps", [("auto", 7), ("fused_tma", 6)])
-def test_asuca_random_state_non_default_constants(coracle, kernel, steps):
+@pytest.mark.parametrize("kernel,steps,wave", [("auto", 7, "0"), ("fused_tma", 6, "0"),
+                                               ("fused_tma", 6, "1")])
+def test_asuca_random_state_non_default_constants(coracle, kernel, steps, wave, monkeypatch):
     """BASELINE's full size from a random state with non-default constants: the
-    pair passes (auto) and the multi-step launch (fused_tma), bitwise."""
+    pair passes (auto), one launch per step (fused_tma) and the multi-step launch
+    (fused_tma, HFTW_WAVE=1: at this size AUTO prefers one launch per step), bitwise."""
+    monkeypatch.setenv("HFTW_WAVE", wave)
     rng = np.random.default_rng(1802)
     cfg = W.GridConfig(nx=1581, ny=1301, nz=58, diffusion_velocity=0.1375,
                        radiation_intensity=-0.21, transfer_velocity=0.047,
