@@ -146,7 +146,7 @@ __device__ __forceinline__ void inter_inner(const IRow& r, double* out, double* 
     const double* p0 = r.e0 + (kl - 1) * W;
     const double* pm = r.em + (kl - 1) * W;
     const double* pp = r.ep + (kl - 1) * W;
-    double* q = ib ? ib + (kl - 1) * kPairIC : nullptr;
+    double* q = ib + (kl - 1) * kPairIC; // ib: this row's buffer, never null here
     auto corr = [&](double x, double bnd) { return dsub(x, dmul(tv, dsub(x, bnd))); };
     const double* sfr = r.S0;     // sf row (pb is W further)
     // window: pd = P(k-1), pc = P(k).  The fast shapes are used only when every
@@ -187,10 +187,8 @@ __device__ __forceinline__ void inter_inner(const IRow& r, double* out, double* 
     // row-buffer stores after the loop: a store inside it would keep the
     // compiler from hoisting the next plane's slab loads above it (possible
     // shared-memory aliasing), serialising the planes
-    if (ib) {
 #pragma unroll
-        for (int kk = 0; kk < NK; ++kk) q[kk * kPairIC] = out[kk];
-    }
+    for (int kk = 0; kk < NK; ++kk) q[kk * kPairIC] = out[kk];
 }
 
 // Generic (any plane range, runtime nk <= KP): Pfull everywhere.  Used only
