@@ -466,11 +466,17 @@ def e2e(ctx, sim, cfg, args, stream, world):
     import torch
     n3 = (cfg.nx + 2) * (cfg.ny + 2) * cfg.nz
     n2 = (cfg.nx + 2) * (cfg.ny + 2)
-    pinned = world == 1
-    mk = ((lambda n: torch.empty(n, dtype=torch.float64, pin_memory=True).numpy()) if pinned
-          else (lambda n: __import__("numpy").empty(n)))
-    bufs = {n: mk(n3 if n in ("energy", "energy_u") else n2)
-            for n in ("energy", "energy_u", "energy_surf", "energy_pbl")}
+    def mk(n, pin):
+        return (torch.empty(n, dtype=torch.float64, pin_memory=True).numpy() if pin
+                else __import__("numpy").empty(n))
+
+    names = ("energy", "energy_u", "energy_surf", "energy_pbl")
+    try:
+        bufs = {n: mk(n3 if n in ("energy", "energy_u") else n2, True) for n in names}
+        pinned = True
+    except RuntimeError:  # a decomposed run's ranks each hold the global host arrays
+        bufs = {n: mk(n3 if n in ("energy", "energy_u") else n2, False) for n in names}
+        pinned = False
     for n in bufs:
         ctx.download(n, bufs[n])
     K = max(1, args.e2e_steps)
@@ -515,9 +521,10 @@ def e2e(ctx, sim, cfg, args, stream, world):
             "ms_per_step": ms, "wall_ms_per_step": wall / K * 1e3,
             "api": ("hftw_step_host (reference_step on a host SimState: H2D of energy/"
                     "energy_surf/energy_pbl, the step, D2H of energy/energy_u, pipelined in "
-                    "row blocks), pinned host buffers"
-                    if pinned else "per rank: hftw_upload x3 (owned part) + hftw_exchange + "
-                    "hftw_step(1) + hftw_download x2 (owned part), pageable host buffers")}
+                    "row blocks)" if sim is None else
+                    "per rank: hftw_upload x3 (owned part) + hftw_exchange + hftw_step(1) + "
+                    "hftw_download x2 (owned part)") +
+                   (", pinned host buffers" if pinned else ", pageable host buffers (pinning failed)")}
 
 
 def e2e_run(ctx, cfg, args, stream):
