@@ -21,6 +21,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
+#include <utility>
 #include <string>
 #include <vector>
 
@@ -280,16 +282,30 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
+// A kernel's dynamic shared-memory limit is a per-device property of the
+// function, shared by every context in the process: only ever RAISE it, so a
+// context with a smaller tile (another nz) cannot shrink the limit below what
+// another context's launches request.
+cudaError_t raise_smem_attr(const void* fn, size_t bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, size_t> cur;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& have = cur[{dev, fn}];
+    if (bytes <= have) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess) have = bytes;
+    return e;
+}
+
 template <int TX>
 void set_tma_attrs(size_t smem) {
-    cudaFuncSetAttribute(hftw::step_tma_kernel<TX, kNCW, true, false>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(hftw::step_tma_kernel<TX, kNCW, false, false>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(hftw::step_tma_kernel<TX, kNCW, true, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    cudaFuncSetAttribute(hftw::step_tma_kernel<TX, kNCW, false, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    raise_smem_attr((const void*)hftw::step_tma_kernel<TX, kNCW, true, false>, smem);
+    raise_smem_attr((const void*)hftw::step_tma_kernel<TX, kNCW, false, false>, smem);
+    raise_smem_attr((const void*)hftw::step_tma_kernel<TX, kNCW, true, true>, smem);
+    raise_smem_attr((const void*)hftw::step_tma_kernel<TX, kNCW, false, true>, smem);
 }
 
 // Choose the TMA kernel geometry and build the tensor maps.  Leaves
@@ -451,8 +467,7 @@ int setup_pair(hftw_ctx* c) {
     if (!ns) return HFTW_OK;
     c->pair_ns = ns;
     c->pair_smem = hftw::pair_smem_bytes(nz, ns);
-    CUDA_TRY(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)c->pair_smem));
+    CUDA_TRY(c, raise_smem_attr((const void*)kern, c->pair_smem));
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, hftw::kPairThreads,
                                                       c->pair_smem) != cudaSuccess ||
@@ -587,8 +602,7 @@ int setup_wave(hftw_ctx* c) {
     if (!c->tma_ok || c->layout != HFTW_IJK || c->tx != 64 || env_int("HFTW_NO_WAVE", 0))
         return HFTW_OK;
     auto kern = hftw::step_wave_kernel<64, kNCW>;
-    CUDA_TRY(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)c->smem));
+    CUDA_TRY(c, raise_smem_attr((const void*)kern, c->smem));
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (kNCW + 1) * 32, c->smem) !=
             cudaSuccess ||
@@ -1438,12 +1452,7 @@ int hftw_flush_l2(hftw_ctx* c, size_t bytes) {
         CUDA_TRY(c, cudaMalloc(&c->flush_buf, bytes));
         c->flush_bytes = bytes;
     }
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(hftw::flush_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             200 * 1024);
-        attr = true;
-    }
+    raise_smem_attr((const void*)hftw::flush_kernel, 200 * 1024);
     const size_t dyn = c->tma_ok ? std::min<size_t>(c->smem, 200 * 1024) : 0;
     hftw::flush_kernel<<<c->num_sms, 512, dyn, c->stream>>>(
         static_cast<double4*>(c->flush_buf), (long long)(bytes / 32), 1.0);

@@ -389,3 +389,35 @@ def test_physics_phase_vs_oracle(coracle, shape, layout, mode):
         got = ctx.download("energy")
     bad = np.flatnonzero(got != want)
     assert bad.size == 0, (shape, layout, mode, bad[:5])
+
+
+def test_concurrent_contexts_vs_oracle(coracle):
+    """Two contexts on their own streams run pair passes and multi-step launches at the
+    same time (each persistent grid takes whatever SMs it gets; the work-unit counters
+    are per context): both bitwise."""
+    cases = []
+    for seed, shape, kernel in ((11, (300, 210, 58), "auto"), (12, (257, 190, 40), "fused_tma")):
+        rng = np.random.default_rng(seed)
+        nx, ny, nz = shape
+        cfg = W.GridConfig(nx=nx, ny=ny, nz=nz, diffusion_velocity=float(rng.uniform(0, 1 / 6)),
+                           radiation_intensity=float(rng.uniform(-0.5, 0.5)),
+                           transfer_velocity=float(rng.uniform(0, 0.1)))
+        g = O.grid_from(cfg)
+        n3, n2 = O.shapes(g)
+        s0 = O.State(rng.uniform(150, 350, n3), rng.uniform(150, 350, n3),
+                     rng.uniform(150, 350, n2), rng.uniform(150, 350, n2))
+        cases.append((cfg, kernel, s0, coracle.steps(g, s0, 9).fields()))
+    ctxs = [W.Context(cfg, kernel=kernel) for cfg, kernel, _, _ in cases]
+    try:
+        for ctx, (_, _, s0, _) in zip(ctxs, cases):
+            for name, arr in s0.fields().items():
+                ctx.upload(name, np.ascontiguousarray(arr))
+        for _ in range(3):          # interleaved, asynchronous: the launches overlap
+            for ctx in ctxs:
+                ctx.step(3)
+        for ctx, (cfg, kernel, _, want) in zip(ctxs, cases):
+            got = {n: ctx.download(n) for n in ("energy", "energy_u", "energy_surf", "energy_pbl")}
+            assert_same(got, want, f"concurrent/{kernel}")
+    finally:
+        for ctx in ctxs:
+            ctx.close()
