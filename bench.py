@@ -183,7 +183,8 @@ def run_reference_arm(args):
     rate, dt, kind, sample = cpu_reference_rate(grid, n, args.workload)
     line = {"metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
             "steps": n, "warmup": args.warmup, "ms_per_step": dt / n * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "weak" if world == 1 else args.scaling,
+            "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference_init initial condition)", "impl": "reference",
             "config": {"workload": desc, "grid": list(grid), "cells_counted": "inner nx*ny*nz"},
             "cpu_baseline": {"value": rate, "unit": UNIT, "cores": 1, "kind": kind,
