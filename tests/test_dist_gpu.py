@@ -24,11 +24,13 @@ def free_port():
     return p
 
 
-def _worker(rank, world, port, shape, grid, steps, layout, kernel, random_init, q):
+def _worker(rank, world, port, shape, grid, steps, layout, kernel, random_init, q, env=None,
+            calls=None):
     import torch.distributed as dist
     from paper_1802_05839_b200.dist import DistSimulation
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
+    os.environ.update(env or {})
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         nx, ny, nz = shape
@@ -48,9 +50,12 @@ def _worker(rank, world, port, shape, grid, steps, layout, kernel, random_init, 
         else:
             s0 = O.COracle().init(g)
             sim.init()
-        half = steps // 2
-        sim.step(half)
-        sim.step(steps - half)
+        if calls is None:
+            half = steps // 2
+            calls = [half, steps - half]
+        assert sum(calls) == steps
+        for n in calls:
+            sim.step(n)
         sim.sync()
         st = sim.gather_state(0)
         if rank == 0:
@@ -74,13 +79,30 @@ def _worker(rank, world, port, shape, grid, steps, layout, kernel, random_init, 
     ((200, 140, 20), (2, 4), 9, "ijk", "auto", True),
 ])
 def test_decomposed_gpu_bitwise(shape, grid, steps, layout, kernel, random_init):
+    _run_decomposed(shape, grid, steps, layout, kernel, random_init)
+
+
+@pytest.mark.parametrize("shape,grid,calls,env", [
+    # one launch per step for every call (what a large rank uses), mixed call lengths
+    ((131, 97, 12), (2, 2), [1, 3, 1, 2], {"HFTW_NO_WAVE": "1"}),
+    ((150, 70, 58), (1, 2), [2, 1, 4], {"HFTW_NO_WAVE": "1"}),
+    # single steps and multi-step launches interleaved on the same step flags
+    ((131, 97, 12), (2, 2), [1, 4, 1, 3, 2], {}),
+    ((120, 90, 20), (2, 4), [3, 1, 5], {"HFTW_WAVE": "1"}),
+])
+def test_decomposed_call_mix_bitwise(shape, grid, calls, env):
+    _run_decomposed(shape, grid, sum(calls), "ijk", "fused_tma", True, env, calls)
+
+
+def _run_decomposed(shape, grid, steps, layout, kernel, random_init, env=None, calls=None):
     import torch.multiprocessing as mp
     world = grid[0] * grid[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, shape, grid, steps, layout, kernel,
-                                               random_init, q)) for r in range(world)]
+                                               random_init, q, env, calls))
+             for r in range(world)]
     for p in procs:
         p.start()
     for p in procs:
