@@ -381,7 +381,10 @@ def run_ours(args):
                        for n, k in kinds.items())
     else:
         dom, dom_name = None, kernel_name
-        avg_launch_s = statistics.mean(launch_ms) * 1e-3
+        # physics / stencil: one launch per call; back to back (no flush) its duration
+        # is the timed region over the calls (launch gaps included), as for `value`
+        avg_launch_s = (total_ms / K if flush is None and not whole
+                        else statistics.mean(launch_ms)) * 1e-3
         launches = K * (ctx.launches_per_step if args.workload == "full" else 1)
     achieved = alg_bytes / avg_launch_s / 1e9
     tkey = f"mode{args.physics_mode}" if args.workload == "physics" else dom_name
@@ -412,6 +415,8 @@ def run_ours(args):
                          "algorithmic_bytes_per_launch": alg_bytes,
                          "steps_per_launch": kinds[dom]["steps_per_launch"] if dom else 1,
                          "avg_launch_ms": avg_launch_s * 1e3,
+                         "avg_launch_ms_events": (statistics.mean(launch_ms)
+                                                  if not whole else None),
                          "algorithmic_bytes_per_cell_step": 16,
                          "note": ("pair passes compute two steps per HBM pass (the intermediate "
                                   "field stays in shared memory/registers): DRAM traffic is "
