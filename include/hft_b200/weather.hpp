@@ -23,6 +23,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cstring>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -164,17 +165,52 @@ void reference_init(const Cfg& cfg, State& st, int device = 0) {
     s.download(st);
 }
 
+namespace detail {
+/// The context reference_step runs on: one per host thread, kept between
+/// calls while the grid (all ten GridConfig fields) and device stay the same,
+/// so a loop of reference_step calls pays the device allocation once.
+struct CachedSim {
+    hftw_grid key{};
+    int device = -1;
+    hftw_ctx* ctx = nullptr;
+    ~CachedSim() { reset(); }
+    void reset() {
+        if (ctx) hftw_destroy(ctx);
+        ctx = nullptr;
+        device = -1;
+    }
+    hftw_ctx* get(const hftw_grid& g, int dev) {
+        if (!ctx || dev != device || std::memcmp(&g, &key, sizeof g) != 0) {
+            reset();
+            check(hftw_create(&g, HFTW_IJK, dev, &ctx));
+            key = g;
+            device = dev;
+        }
+        return ctx;
+    }
+};
+inline CachedSim& cached_sim() {
+    thread_local CachedSim c;
+    return c;
+}
+} // namespace detail
+
+/// Free the context that reference_step keeps for this host thread.
+inline void release_cached_context() { detail::cached_sim().reset(); }
+
 /// hft::reference_step (weather.cpp:101-171) on a host SimState, in place.
 /// Transfer-bound by construction (hftw_step_host overlaps the PCIe copies
 /// with the step in row blocks); keep state on the device (Simulation) for
-/// runs of more than one step.
+/// runs of more than one step.  The device context is reused across calls
+/// on the same grid (release_cached_context frees it).
 template <class Cfg, class State>
 void reference_step(const Cfg& cfg, State& st, int device = 0) {
-    Simulation s(cfg, HFTW_IJK, device);
-    check(hftw_step_host(s.handle(), st.energy.data.data(), st.energy_surf.data.data(),
+    const hftw_grid g = to_grid(cfg);
+    hftw_ctx* ctx = detail::cached_sim().get(g, device);
+    check(hftw_step_host(ctx, st.energy.data.data(), st.energy_surf.data.data(),
                          st.energy_pbl.data.data(), st.energy.data.data(),
                          st.energy_u.data.data()),
-          s.handle());
+          ctx);
 }
 
 /// hft::run_reference (weather.cpp:173-178).

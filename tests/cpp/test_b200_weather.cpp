@@ -95,6 +95,22 @@ int main() {
             hft::b200::reference_step(cfg, mine);
         }
         CHECK(bitwise(st, mine, "reference_step x3"));
+        // two grids in turn: the cached device context follows the config
+        hft::GridConfig cfg2 = cfg;
+        cfg2.nx = 40;
+        cfg2.radiation_intensity = -0.2;
+        hft::SimState st2, mine2;
+        hft::reference_init(cfg2, st2);
+        mine2 = st2;
+        for (int n = 0; n < 3; ++n) {
+            hft::reference_step(cfg, st);
+            hft::b200::reference_step(cfg, mine);
+            hft::reference_step(cfg2, st2);
+            hft::b200::reference_step(cfg2, mine2);
+        }
+        CHECK(bitwise(st, mine, "reference_step, alternating grids (1)"));
+        CHECK(bitwise(st2, mine2, "reference_step, alternating grids (2)"));
+        hft::b200::release_cached_context();
     }
     // the device-resident API: every step kernel, both layouts
     {
