@@ -27,6 +27,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import threading
 from dataclasses import dataclass, fields
 from dataclasses import field as dc_field
 from typing import Dict, List, Optional, Sequence, Tuple
@@ -38,8 +39,9 @@ from ._lib import HftwError, check, hftw_grid, lib
 
 __all__ = [
     "GridConfig", "Diagnostics", "validate", "ArrayObject", "SimState", "reference_init",
-    "reference_step", "run_reference", "CompareReport", "StateReport", "compare_arrays",
-    "compare_fields", "dump_field", "read_field", "unpermute_storage", "Context", "HftwError",
+    "reference_step", "release_cached_context", "run_reference", "CompareReport", "StateReport",
+    "compare_arrays", "compare_fields", "dump_field", "read_field", "unpermute_storage", "Context",
+    "HftwError",
 ]
 
 
@@ -389,16 +391,33 @@ def reference_init(cfg: GridConfig, st: SimState, device: int = 0) -> None:
         new.energy, new.energy_u, new.energy_surf, new.energy_pbl)
 
 
+_cached = threading.local()  # reference_step's context, per host thread
+
+
+def release_cached_context() -> None:
+    """Free the device context reference_step keeps for this thread."""
+    ctx = getattr(_cached, "ctx", None)
+    if ctx is not None:
+        ctx.close()
+    _cached.ctx, _cached.key = None, None
+
+
 def reference_step(cfg: GridConfig, st: SimState, device: int = 0) -> None:
     """hft::reference_step (weather.cpp:101-171) on a host SimState, in place.
 
     Drop-in but transfer-bound (hftw_step_host pipelines the PCIe copies with
-    the kernels); keep the state on the device with ``Context`` for real runs."""
-    with Context(cfg, device=device) as ctx:
-        e = np.ascontiguousarray(st.energy.data, dtype=np.float64)
-        eu = np.empty_like(e)
-        ctx.step_host(e, np.ascontiguousarray(st.energy_surf.data, dtype=np.float64),
-                      np.ascontiguousarray(st.energy_pbl.data, dtype=np.float64), e, eu)
+    the kernels); keep the state on the device with ``Context`` for real runs.
+    The device context is reused between calls on the same grid and device
+    (``release_cached_context`` frees it)."""
+    key = (tuple(getattr(cfg, f.name) for f in fields(cfg)), device)
+    if getattr(_cached, "key", None) != key:
+        release_cached_context()
+        _cached.ctx, _cached.key = Context(cfg, device=device), key
+    ctx = _cached.ctx
+    e = np.ascontiguousarray(st.energy.data, dtype=np.float64)
+    eu = np.empty_like(e)
+    ctx.step_host(e, np.ascontiguousarray(st.energy_surf.data, dtype=np.float64),
+                  np.ascontiguousarray(st.energy_pbl.data, dtype=np.float64), e, eu)
     st.energy = ArrayObject(st.energy.bounds, e)
     st.energy_u = ArrayObject(st.energy_u.bounds, eu)
 

@@ -210,6 +210,26 @@ def test_reference_api_mirror(coracle):
     assert np.array_equal(s2.energy.data, coracle.run_reference(g, 1).energy)
 
 
+def test_reference_step_loop_two_grids(coracle):
+    """reference_step in a loop, alternating two grids: the cached per-thread context
+    follows the config; bitwise against the oracle."""
+    cfgs = [W.GridConfig(nx=21, ny=13, nz=7), W.GridConfig(nx=30, ny=11, nz=9,
+                                                           radiation_intensity=-0.3)]
+    sts = []
+    for cfg in cfgs:
+        st = W.SimState.allocate(cfg)
+        W.reference_init(cfg, st)
+        sts.append(st)
+    for _ in range(3):
+        for cfg, st in zip(cfgs, sts):
+            W.reference_step(cfg, st)
+    W.release_cached_context()
+    for cfg, st in zip(cfgs, sts):
+        want = coracle.run_reference(O.grid_from(cfg), 3)
+        assert np.array_equal(st.energy.data, want.energy)
+        assert np.array_equal(st.energy_u.data, want.energy_u)
+
+
 def test_errors_are_loud():
     with pytest.raises(W.HftwError):
         with W.Context(W.GridConfig(nz=300)) as ctx:
