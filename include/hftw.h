@@ -122,6 +122,14 @@ int hftw_step(hftw_ctx* ctx, int64_t nsteps);
 int hftw_step_host(hftw_ctx* ctx, const double* energy, const double* energy_surf,
                    const double* energy_pbl, double* energy_out, double* energy_u_out);
 
+/* Page-lock (and unlock) host memory the caller owns, e.g. the four
+ * std::vector buffers of a SimState, so that hftw_step_host / upload /
+ * download move it at PCIe speed: pageable buffers go through the driver's
+ * bounce buffer (ASUCA reference_step: ~185 ms against ~41 ms pinned).  The
+ * range must stay allocated until hftw_host_unregister. */
+int hftw_host_register(void* ptr, size_t bytes);
+int hftw_host_unregister(void* ptr);
+
 /* Wait for all work queued on the context stream. */
 int hftw_sync(hftw_ctx* ctx);
 

@@ -74,6 +74,8 @@ SIGNATURES = [
     ("hftw_download", C.c_int, [_P, C.c_int, _D]),
     ("hftw_step", C.c_int, [_P, C.c_int64]),
     ("hftw_step_host", C.c_int, [_P, _D, _D, _D, _D, _D]),
+    ("hftw_host_register", C.c_int, [C.c_void_p, C.c_size_t]),
+    ("hftw_host_unregister", C.c_int, [C.c_void_p]),
     ("hftw_sync", C.c_int, [_P]),
     ("hftw_set_timing", C.c_int, [_P, C.c_int]),
     ("hftw_get_timing", C.c_int, [_P, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_int64),

@@ -1673,6 +1673,22 @@ int hftw_simulate(hftw_ctx* c, double start_time, double end_time, double timest
     return HFTW_OK;
 }
 
+int hftw_host_register(void* ptr, size_t bytes) {
+    if (!ptr || !bytes) return fail(nullptr, HFTW_EINVAL, "null or empty host range");
+    const cudaError_t e = cudaHostRegister(ptr, bytes, cudaHostRegisterPortable);
+    if (e != cudaSuccess)
+        return fail(nullptr, HFTW_ECUDA, "cudaHostRegister failed: %s", cudaGetErrorString(e));
+    return HFTW_OK;
+}
+
+int hftw_host_unregister(void* ptr) {
+    if (!ptr) return fail(nullptr, HFTW_EINVAL, "null host pointer");
+    const cudaError_t e = cudaHostUnregister(ptr);
+    if (e != cudaSuccess)
+        return fail(nullptr, HFTW_ECUDA, "cudaHostUnregister failed: %s", cudaGetErrorString(e));
+    return HFTW_OK;
+}
+
 int hftw_step_host(hftw_ctx* c, const double* energy, const double* energy_surf,
                    const double* energy_pbl, double* energy_out, double* energy_u_out) {
     int rc = check_ctx(c);

@@ -110,6 +110,14 @@ int main() {
         }
         CHECK(bitwise(st, mine, "reference_step, alternating grids (1)"));
         CHECK(bitwise(st2, mine2, "reference_step, alternating grids (2)"));
+        {   // page-locked SimState buffers (hftw_host_register), same results
+            hft::b200::PinnedState pin(mine);
+            for (int n = 0; n < 2; ++n) {
+                hft::reference_step(cfg, st);
+                hft::b200::reference_step(cfg, mine);
+            }
+            CHECK(bitwise(st, mine, "reference_step, pinned SimState"));
+        }
         hft::b200::release_cached_context();
     }
     // the device-resident API: every step kernel, both layouts

@@ -230,6 +230,23 @@ def test_reference_step_loop_two_grids(coracle):
         assert np.array_equal(st.energy_u.data, want.energy_u)
 
 
+def test_reference_step_pinned_state(coracle):
+    """reference_step on page-locked SimState buffers (weather.pinned): bitwise, and the
+    buffers are written in place."""
+    cfg = W.GridConfig(nx=40, ny=25, nz=12, diffusion_velocity=0.15)
+    st = W.SimState.allocate(cfg)
+    W.reference_init(cfg, st)
+    with W.pinned(st):
+        e0, eu0 = st.energy.data, st.energy_u.data
+        for _ in range(2):
+            W.reference_step(cfg, st)
+        assert st.energy.data is e0 and st.energy_u.data is eu0
+    W.release_cached_context()
+    want = coracle.run_reference(O.grid_from(cfg), 2)
+    assert np.array_equal(st.energy.data, want.energy)
+    assert np.array_equal(st.energy_u.data, want.energy_u)
+
+
 def test_errors_are_loud():
     with pytest.raises(W.HftwError):
         with W.Context(W.GridConfig(nz=300)) as ctx:
