@@ -86,6 +86,10 @@ def test_decomposed_gpu_bitwise(shape, grid, steps, layout, kernel, random_init)
     # one launch per step for every call (what a large rank uses), mixed call lengths
     ((131, 97, 12), (2, 2), [1, 3, 1, 2], {"HFTW_NO_WAVE": "1"}),
     ((150, 70, 58), (1, 2), [2, 1, 4], {"HFTW_NO_WAVE": "1"}),
+    # odd process grids (uneven partitions, a rank between two others in both directions)
+    ((97, 61, 13), (3, 1), [2, 3], {}),
+    ((61, 97, 13), (1, 3), [1, 4], {}),
+    ((100, 70, 9), (3, 2), [3, 2], {}),
     # single steps and multi-step launches interleaved on the same step flags
     ((131, 97, 12), (2, 2), [1, 4, 1, 3, 2], {}),
     ((120, 90, 20), (2, 4), [3, 1, 5], {"HFTW_WAVE": "1"}),
