@@ -47,7 +47,7 @@ int env_int(const char* name, int dflt) {
 constexpr int kFrontPad = 31; // IJK: logical i = 1 lands on a 256-byte boundary
 constexpr int kNCW = 16;      // consumer warps of the TMA kernel
 constexpr int kChunk = 32;    // rows per TMA work unit
-constexpr int kMaxPipeBlocks = 32; // row blocks of the hftw_step_host pipeline
+constexpr int kMaxPipeBlocks = 64; // row blocks of the hftw_step_host pipeline (at most)
 constexpr int kMaxWaveStepsDist = 1024; // steps per multi-step launch when decomposed
 #ifndef HFTW_PAIR_KPT
 #define HFTW_PAIR_KPT (64 / HFTW_PAIR_KG)
@@ -1720,12 +1720,13 @@ int hftw_step_host(hftw_ctx* c, const double* energy, const double* energy_surf,
     // the kernels and D2H overlap (PCIe is full duplex).  In-place use
     // (energy_out == energy) is safe: a row is read back only after every row
     // has been uploaded up to its j+1 neighbour.
-    const int nb = std::max(1, std::min(c->nchunks, std::min(kMaxPipeBlocks, env_int("HFTW_PIPE_BLOCKS", kMaxPipeBlocks))));
+    const int nb = std::max(
+        1, std::min(c->nchunks, std::min(kMaxPipeBlocks, env_int("HFTW_PIPE_BLOCKS", 32))));
     if (!c->h2d_stream) {
         CUDA_TRY(c, cudaStreamCreateWithFlags(&c->h2d_stream, cudaStreamNonBlocking));
         CUDA_TRY(c, cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking));
     }
-    while ((int)c->pipe_ev.size() < 2 * kMaxPipeBlocks + 2) {
+    while ((int)c->pipe_ev.size() < 3 * kMaxPipeBlocks + 2) {
         cudaEvent_t e;
         CUDA_TRY(c, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         c->pipe_ev.push_back(e);
@@ -1739,7 +1740,8 @@ int hftw_step_host(hftw_ctx* c, const double* energy, const double* energy_surf,
     double* const seu = c->host_stage[2];
     cudaEvent_t* evH = c->pipe_ev.data();
     cudaEvent_t* evC = evH + kMaxPipeBlocks;
-    cudaEvent_t evStart = evH[2 * kMaxPipeBlocks], evG = evH[2 * kMaxPipeBlocks + 1];
+    cudaEvent_t* evU = evH + 2 * kMaxPipeBlocks;
+    cudaEvent_t evStart = evH[3 * kMaxPipeBlocks], evG = evH[3 * kMaxPipeBlocks + 1];
     const int src = c->cur;
     // earlier work on the context stream (steps reading buf[src]) comes first
     CUDA_TRY(c, cudaEventRecord(evStart, c->stream));
@@ -1781,23 +1783,36 @@ int hftw_step_host(hftw_ctx* c, const double* energy, const double* energy_surf,
         CUDA_TRY(c, cudaGetLastError());
         return HFTW_OK;
     };
-    if ((rc = scatter(0))) return rc;
+    // energy_u of block b (physics of its input rows) needs only block b itself,
+    // so it is computed right after the scatter and its D2H goes out one block
+    // ahead of the new rows: the D2H stream starts earlier and drains sooner
+    auto physics_rows = [&](int b) -> int {
+        const long long r0 = row_lo(b), r1 = row_hi(b);
+        hftw::physics_copy_kernel<<<grid_rows(r0, r1), 256, 0, c->stream>>>(
+            e3(c, src), seu, hsj, hsk, sf2(c), pb2(c), d, (int)r0, (int)r1);
+        CUDA_TRY(c, cudaGetLastError());
+        CUDA_TRY(c, cudaEventRecord(evU[b], c->stream));
+        return HFTW_OK;
+    };
+    auto eu_out = [&](int b) -> int {
+        CUDA_TRY(c, cudaStreamWaitEvent(c->d2h_stream, evU[b], 0));
+        return pcie(energy_u_out, seu, row_lo(b), row_hi(b), cudaMemcpyDeviceToHost,
+                    c->d2h_stream);
+    };
+    if ((rc = scatter(0)) || (rc = physics_rows(0)) || (rc = eu_out(0))) return rc;
     for (int b = 0; b < nb; ++b) {
-        if (b + 1 < nb && (rc = scatter(b + 1))) return rc;
+        if (b + 1 < nb && ((rc = scatter(b + 1)) || (rc = physics_rows(b + 1)))) return rc;
         const int ja = chunk_lo(b) * c->chunk + 1;
         const int jb = (int)std::min<long long>(ny, (long long)chunk_lo(b + 1) * c->chunk);
         const StepPart part{chunk_lo(b) * c->nstrips, chunk_lo(b + 1) * c->nstrips, ja, jb, 0};
         if ((rc = launch_fused<true>(c, src, HFTW_KERNEL_FUSED_TMA, &part))) return rc;
-        const long long r0 = row_lo(b), r1 = row_hi(b);
-        hftw::physics_copy_kernel<<<grid_rows(r0, r1), 256, 0, c->stream>>>(
-            e3(c, src), seu, hsj, hsk, sf2(c), pb2(c), d, (int)r0, (int)r1);
         hftw::copy_rows_kernel<<<grid_rows(ja, jb), 256, 0, c->stream>>>(
             e3(c, src ^ 1), c->sj, c->sk, sout, hsj, hsk, d, ja, jb);
         CUDA_TRY(c, cudaGetLastError());
         CUDA_TRY(c, cudaEventRecord(evC[b], c->stream));
+        if (b + 1 < nb && (rc = eu_out(b + 1))) return rc;
         CUDA_TRY(c, cudaStreamWaitEvent(c->d2h_stream, evC[b], 0));
-        if ((rc = pcie(energy_out, sout, ja, jb, cudaMemcpyDeviceToHost, c->d2h_stream)) ||
-            (rc = pcie(energy_u_out, seu, r0, r1, cudaMemcpyDeviceToHost, c->d2h_stream)))
+        if ((rc = pcie(energy_out, sout, ja, jb, cudaMemcpyDeviceToHost, c->d2h_stream)))
             return rc;
     }
     const StepPart ghosts{0, 0, 1, 0, 3};
