@@ -23,7 +23,8 @@
 //   * after a barrier, row j = jr-1 of e_{s+2} is computed for the 30 columns
 //     i0 .. i0+29: the i and j-1 neighbours from the row buffers, the centre,
 //     its k neighbours and the j+1 neighbour from this thread's registers --
-//     and stored straight to HBM.  A second barrier frees the oldest buffer.
+//     and stored straight to HBM.  One CTA barrier per row: the buffer the
+//     next row overwrites is read in this final row only by its own thread.
 //   * the edge planes k = 1 and nz (physics corrections, k-plane formulas)
 //     are peeled at compile time per k-group "shape", so the common planes
 //     run without them.
