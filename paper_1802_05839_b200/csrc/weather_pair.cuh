@@ -15,7 +15,7 @@
 //     one box the sf and pb rows, and -- for the two edge strips -- a 2-wide
 //     box holds the cyclic partner column of the i-ghost cell (column nx for
 //     strip 0, column 1 for the last strip).  Thread 0 refills the ring slot
-//     a row frees right after the row's first barrier (no producer warp);
+//     a row frees right after the row's barrier (no producer warp);
 //   * row jr of the intermediate P' = physics(e_{s+1}) is computed for the 32
 //     columns i0-1 .. i0+30 from slabs jr-1, jr, jr+1: 8 k-groups of 7-8
 //     planes x 32 columns = 8 warps, each thread walking its planes with a
