@@ -3,6 +3,8 @@ the 1-2 cell edge cases and odd nz), random physical constants, random initial f
 1-7 steps in one call and as separate calls, every kernel and layout the context
 accepts.  Bitwise, like tests/test_parity_gpu.py; the case list is fixed by the seed so
 a failure reproduces by its id."""
+import os
+
 import numpy as np
 import pytest
 
@@ -14,7 +16,7 @@ pytestmark = pytest.mark.gpu
 KERNELS = ["auto", "fused_tma", "fused_pair", "fused_cell", "split"]
 
 
-def cases(n=160, seed=20261017):
+def cases(n=160, seed=int(os.environ.get("HFTW_FUZZ_SEED", "20261017"))):
     rng = np.random.default_rng(seed)
     out = []
     for c in range(n):

@@ -4,6 +4,8 @@ the middle (energy_u is derived lazily from the previous field and sf/pb, so a n
 must not change an energy_u that belongs to an earlier step), and downloads at random
 points.  Bitwise.  The library state machine under test: the ping-pong buffer index,
 the lazily derived energy_u, the pair / multi-step / single-step launch choice."""
+import os
+
 import numpy as np
 import pytest
 
@@ -38,7 +40,7 @@ class Model:
         self.f["energy"] = u
 
 
-def sequences(n=120, seed=1802):
+def sequences(n=120, seed=int(os.environ.get("HFTW_FUZZ_SEED", "1802"))):
     rng = np.random.default_rng(seed)
     kernels = ["auto", "fused_tma", "fused_pair", "fused_cell", "split"]
     out = []
