@@ -9,6 +9,12 @@ larger than the 126 MB L2, so no flush is needed between steps).
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                   [--workload full|stencil|physics] [--layout ijk|kij] [--kernel auto|...]
 
+--gpus N > 1 runs the paper's I x J decomposition (2 -> 2x1, 4 -> 2x2, 8 -> 2x4):
+  * under torchrun (WORLD_SIZE set): one process per GPU, halos pushed by the
+    step kernels through CUDA IPC mappings;
+  * without it: ONE process drives N devices (hftw_create_multi, peer access
+    over NVLink).  It exits non-zero when fewer than N GPUs are visible.
+
 "value" counts INNER cells (nx*ny*nz per step), the convention BASELINE.md
 uses for the paper's numbers.  The roofline uses SURVEY.md 8(d)'s
 algorithmic bytes: 16 B per stored cell + 16 B per column for a step.
@@ -34,13 +40,10 @@ sys.path.insert(0, ROOT)
 METRIC = "grid-cell updates/sec per timestep and achieved HBM GB/s vs peak"
 UNIT = "cell-updates/s"
 WORKLOADS = {
-    # name: (grid, description)
-    "full": ((1581, 1301, 58), "full minimal-weather timestep (column physics + 7-point "
-             "diffusion, cyclic ghosts) on the ASUCA grid 1581x1301x58 fp64, single B200"),
-    "stencil": ((256, 256, 64), "3D diffusion stencil only, 256x256x64 fp64 (L2 cold: "
-                "independent grids swept round robin, or an L2 flush between sweeps)"),
-    "physics": ((1581, 1301, 58), "column physics only (k-dependent column loop), "
-                "1581x1301x58 fp64"),
+    # name: (grid, short description; the driver truncates long strings)
+    "full": ((1581, 1301, 58), "full timestep (physics + diffusion), ASUCA 1581x1301x58 fp64"),
+    "stencil": ((256, 256, 64), "diffusion stencil only, 256x256x64 fp64"),
+    "physics": ((1581, 1301, 58), "column physics only, ASUCA 1581x1301x58 fp64"),
 }
 
 
@@ -128,6 +131,39 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
+def layout_plan(args, n):
+    """(px, py, scaling, global grid, workload text) of an n-GPU run."""
+    from paper_1802_05839_b200.dist import process_grid
+    grid, desc = WORKLOADS[args.workload]
+    nx, ny, nz = grid
+    px, py = (args.px, args.py) if args.px else process_grid(n)
+    scaling = "weak" if n == 1 else args.scaling
+    if n > 1 and scaling == "weak":
+        nx, ny = nx * px, ny * py  # every GPU keeps an ASUCA-sized subdomain
+        desc = f"full timestep, weak: {nx}x{ny}x{nz} fp64 on {px}x{py} (ASUCA per GPU)"
+    elif n > 1:
+        desc = f"full timestep, strong: ASUCA {nx}x{ny}x{nz} fp64 on {px}x{py}"
+    return px, py, scaling, (nx, ny, nz), desc
+
+
+def config_of(args, n, grid, desc, px, py, l2):
+    """The `config` object, identical in both arms for the same arguments."""
+    return {"workload": desc, "grid": list(grid), "layout": args.layout,
+            "cells_counted": "inner nx*ny*nz per step", "l2": l2,
+            "parallelism": f"{px}x{py} I x J decomposition" if n > 1 else "single GPU"}
+
+
+def l2_note(args):
+    if args.workload != "stencil":
+        return "inputs larger than L2 (957 MB per field vs 126 MB L2)"
+    if args.flush == "rotate":
+        return (f"inputs larger than L2: {ROTATE} independent 256x256x64 grids swept round "
+                f"robin ({ROTATE * 68} MB of fields)")
+    if args.flush == "none":
+        return "NOT flushed (diagnostic)"
+    return f"flushed between sweeps (256 MB write, {args.flush})"
+
+
 # ---------------------------------------------------------------------------
 # CPU: the reference (oracle/_ref) or its C restatement -- checker/baseline only
 # ---------------------------------------------------------------------------
@@ -175,18 +211,21 @@ def run_reference_arm(args):
     rank, world, _ = dist_env()
     if world > 1 and rank != 0:
         return 0
-    grid, desc = WORKLOADS[args.workload]
-    # bounded sample: one reference step is ~0.6 s at the ASUCA size on one core
+    n = max(world, args.gpus)
+    px, py, scaling, ggrid, gdesc = layout_plan(args, n)
+    grid, _ = WORKLOADS[args.workload]  # the CPU sample: one ASUCA-sized domain
+    # bounded sample: one reference step is ~0.3-0.6 s at the ASUCA size on one
+    # core; the reference is serial, so its rate does not depend on the grid split
     n = max(1, min(args.steps, 20 if args.workload != "stencil" else 200))
     for _ in range(min(args.warmup, 1)):
         cpu_reference_rate(grid, 1, args.workload)
     rate, dt, kind, sample = cpu_reference_rate(grid, n, args.workload)
     line = {"metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
             "steps": n, "warmup": args.warmup, "ms_per_step": dt / n * 1e3,
-            "higher_is_better": True, "scaling": "weak" if world == 1 else args.scaling,
+            "higher_is_better": True, "scaling": scaling,
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference_init initial condition)", "impl": "reference",
-            "config": {"workload": desc, "grid": list(grid), "cells_counted": "inner nx*ny*nz"},
+            "config": config_of(args, args.gpus, ggrid, gdesc, px, py, l2_note(args)),
             "cpu_baseline": {"value": rate, "unit": UNIT, "cores": 1, "kind": kind,
                              "sample": sample, "host_nproc": os.cpu_count()},
             "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0,
@@ -201,41 +240,50 @@ def run_reference_arm(args):
 def run_ours(args):
     import torch
     from paper_1802_05839_b200 import weather as W
-    from paper_1802_05839_b200.dist import DistSimulation, process_grid
+    from paper_1802_05839_b200.dist import DistSimulation
 
     rank, world, local = dist_env()
+    # --gpus N without torchrun: ONE process drives N devices (a group context)
+    ngroup = args.gpus if world == 1 else 1
+    if ngroup > 1 and torch.cuda.device_count() < ngroup:
+        print(f"bench.py: --gpus {ngroup} needs {ngroup} visible GPUs, found "
+              f"{torch.cuda.device_count()}", file=sys.stderr)
+        return 2
     ndev = max(1, torch.cuda.device_count())
     device = local % ndev  # ranks > GPUs only when testing the protocol on one GPU
     torch.cuda.set_device(device)
     dist = None
+    if world > 1 and args.gpus not in (1, world):
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        return 2
+    n_gpus = max(world, ngroup)
     if world > 1:
         import torch.distributed as dist
         # no data-path collective: gloo carries the one-time IPC descriptors,
         # the barriers and the max-over-ranks of the timings
         dist.init_process_group("gloo")
-        if args.workload != "full":
-            raise SystemExit("multi-GPU runs measure the full timestep only")
-    grid, desc = WORKLOADS[args.workload]
-    nx, ny, nz = grid
-    px, py = (args.px, args.py) if args.px else process_grid(world)
-    scaling = "weak" if world == 1 else args.scaling
-    if world > 1 and scaling == "weak":
-        nx, ny = nx * px, ny * py  # every GPU keeps an ASUCA-sized subdomain
-        desc = (f"full minimal-weather timestep, weak scaling: {nx}x{ny}x{nz} fp64 "
-                f"({px}x{py} ranks of ~1581x1301x58)")
-    elif world > 1:
-        desc = (f"full minimal-weather timestep on the ASUCA grid {nx}x{ny}x{nz} fp64, strong "
-                f"scaling over {px}x{py} B200 (I x J decomposition, in-kernel NVLink halo push)")
+    if n_gpus > 1 and args.workload != "full":
+        raise SystemExit("multi-GPU runs measure the full timestep only")
+    px, py, scaling, (nx, ny, nz), desc = layout_plan(args, n_gpus)
+    grid = (nx, ny, nz)
     cfg = W.GridConfig(nx=nx, ny=ny, nz=nz)
     sim = None
-    if world == 1:
+    if ngroup > 1:
+        ctx = W.Context(cfg, layout=args.layout, kernel=args.kernel, px=px, py=py,
+                        devices=list(range(ngroup)))
+        ctx.init()
+    elif world == 1:
         ctx = W.Context(cfg, layout=args.layout, device=device, kernel=args.kernel)
         ctx.init()
     else:
         sim = DistSimulation(cfg, px, py, layout=args.layout, device=device, kernel=args.kernel)
         sim.init()
         ctx = sim.ctx
-    stream = torch.cuda.ExternalStream(ctx.stream, device=device)
+    # the streams the kernels run on: one per rank of a group, else the context's
+    ranks = [ctx.rank_context(r) for r in range(ngroup)] if ngroup > 1 else [ctx]
+    rstreams = [torch.cuda.ExternalStream(rc.stream, device=(r if ngroup > 1 else device))
+                for r, rc in enumerate(ranks)]
+    stream = rstreams[0]
     kernel_name = ctx.kernel
     flush = None
     rot = []  # stencil, --flush rotate: independent grids swept round robin
@@ -286,16 +334,26 @@ def run_ours(args):
     # passes where it can.  Physics / stencil: one call per sweep.
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(1 if whole else K)]
+    # a group: one event pair per rank, on that rank's device and stream
+    revs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for _ in rstreams[1:]]
     barrier()
+    ctx.sync()
     torch.cuda.synchronize()
     sampler = ClockSampler(device)
     with sampler:
         t_wall = time.perf_counter()
         with torch.cuda.stream(stream):
             if whole:
+                for (a, _), st in zip(revs, rstreams[1:]):
+                    with torch.cuda.device(st.device):
+                        a.record(st)
                 evs[0][0].record(stream)
                 ctx.step(K)
                 evs[0][1].record(stream)
+                for (_, b), st in zip(revs, rstreams[1:]):
+                    with torch.cuda.device(st.device):
+                        b.record(st)
             elif flush is None:
                 # back-to-back calls, one event pair around all K (per-call events
                 # would add their own gaps); per-launch times come from a second pass
@@ -309,12 +367,14 @@ def run_ours(args):
                     evs[i][0].record(stream)
                     one()
                     evs[i][1].record(stream)
-        stream.synchronize()
+        ctx.sync()
         t_wall = time.perf_counter() - t_wall
     torch.cuda.synchronize()
     barrier()
     if flush is None:
         total_ms = evs[0][0].elapsed_time(evs[-1][1])
+        for a, b in revs:  # the slowest rank of a group
+            total_ms = max(total_ms, a.elapsed_time(b))
     if not whole and flush is None:
         # diagnostic pass: the same K calls with events around each (kernel durations)
         with torch.cuda.stream(stream):
@@ -341,7 +401,8 @@ def run_ours(args):
             # 16 B per stored cell + 16 B per column PER STEP, times the
             # steps one launch processes.  A pair pass keeps its intermediate step on
             # chip, so its DRAM traffic (ncu) is about half of this figure.
-            kd["algorithmic_bytes_per_launch"] = ctx.algorithmic_bytes("step") * kd["steps_per_launch"]
+            kd["algorithmic_bytes_per_launch"] = (ranks[0].algorithmic_bytes("step") *
+                                                  kd["steps_per_launch"])
         ctx.set_timing(False)
     if dist is not None:
         t = torch.tensor([total_ms], dtype=torch.float64)
@@ -358,7 +419,7 @@ def run_ours(args):
     value = inner / (ms_per_step * 1e-3)
 
     what = {"full": "step", "physics": "physics", "stencil": "diffuse"}[args.workload]
-    alg_bytes = ctx.algorithmic_bytes(what)  # this rank's stored cells, per launch
+    alg_bytes = ranks[0].algorithmic_bytes(what)  # one GPU's stored cells, per launch
     peak, peak_src = peaks()
     for kd in kinds.values():
         kd["achieved_GBps"] = kd["algorithmic_bytes_per_launch"] / (kd["avg_launch_ms"] * 1e-3) / 1e9
@@ -388,29 +449,31 @@ def run_ours(args):
         launches = K * (ctx.launches_per_step if args.workload == "full" else 1)
     achieved = alg_bytes / avg_launch_s / 1e9
     tkey = f"mode{args.physics_mode}" if args.workload == "physics" else dom_name
-    traffic = ncu_traffic(args.workload, args.layout, tkey) if world == 1 else None
+    traffic = ncu_traffic(args.workload, args.layout, tkey) if n_gpus == 1 else None
     if traffic is not None and dom in ("multi_step", "pair"):
         traffic *= kinds[dom]["steps_per_launch"]  # the capture is stored per step
+    # what HBM actually moved per second: the ncu DRAM bytes of one launch over
+    # the same average launch duration (temporal blocking makes it less than the
+    # algorithmic figure, so `achieved`/`frac` above 1 are NOT HBM utilisation)
+    dram = traffic / avg_launch_s / 1e9 if traffic is not None else None
 
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n_gpus, "steps": K,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (reference_init initial condition; fp64 fields resident in HBM)",
-            "config": {"workload": desc, "grid": [nx, ny, nz], "layout": args.layout,
-                       "kernel": kernel_name, "cells_counted": "inner nx*ny*nz per step",
-                       "l2": (f"flushed between sweeps (256 MB write, {args.flush})"
-                              if flush is not None else
-                              f"inputs larger than L2: {ROTATE} independent 256x256x64 grids "
-                              f"swept round robin ({ROTATE * 68} MB of fields)"
-                              if rot else
-                              "inputs larger than L2 (957 MB per field vs 126 MB L2)"
-                              if args.workload != "stencil" else "NOT flushed (diagnostic)"),
-                       "parallelism": (f"{px}x{py} I x J decomposition" if world > 1
-                                       else "single GPU")},
-            "hbm_gbs": achieved,
+            "config": config_of(args, n_gpus, grid, desc, px, py, l2_note(args)),
+            "kernel": kernel_name,
+            "launcher": ("torchrun: one process per GPU (CUDA IPC halos)" if world > 1 else
+                         "one process, a group context over the GPUs" if ngroup > 1 else
+                         "one process, one GPU"),
+            "hbm_gbs": dram if dram is not None else achieved,
+            "hbm_gbs_source": "ncu DRAM bytes / launch time" if dram is not None else
+                              "algorithmic bytes / launch time (no ncu capture for this config)",
+            "effective_gbs": achieved,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                         "per": "GPU (rank 0)" if world > 1 else "GPU",
+                         "dram_gbs": dram, "dram_frac": dram / peak if dram else None,
+                         "per": "GPU (rank 0)" if n_gpus > 1 else "GPU",
                          "kernel": dom_name,
                          "algorithmic_bytes_per_launch": alg_bytes,
                          "steps_per_launch": kinds[dom]["steps_per_launch"] if dom else 1,
@@ -419,9 +482,10 @@ def run_ours(args):
                                                   if not whole else None),
                          "algorithmic_bytes_per_cell_step": 16,
                          "note": ("pair passes compute two steps per HBM pass (the intermediate "
-                                  "field stays in shared memory/registers): DRAM traffic is "
-                                  "~8 B per cell-step, half the algorithmic 16 B, so frac "
-                                  "measures cell-updates against the 16-B roofline"
+                                  "field stays on chip): DRAM traffic is ~8 B per cell-step, "
+                                  "half the algorithmic 16 B, so frac (> 1) measures cell "
+                                  "updates against a one-step-per-pass kernel at the HBM peak; "
+                                  "dram_frac is the HBM utilisation"
                                   if dom == "pair" else None),
                          "paper_model_bytes_per_cell": {"m_sa=4": 32, "m_sa=10": 80}},
             "kernels": kinds,
@@ -433,20 +497,20 @@ def run_ours(args):
         # the paper's bandwidth model (perfmodel.cpp:141-154) on the measured B200
         # entry, for the same grid: m_sa = 10 / 4 values per cell vs measured
         from paper_1802_05839_b200 import perfmodel
-        lnx, lny = (ctx.plan["lnx"], ctx.plan["lny"]) if world > 1 else (nx, ny)
+        lnx, lny = (ranks[0].plan["lnx"], ranks[0].plan["lny"]) if n_gpus > 1 else (nx, ny)
         rep = perfmodel.b200_report(ms_per_step, lnx, lny, nz)  # per GPU
         line["paper_model"] = {k: rep[k] for k in ("model_ms_per_step", "bw_d_GBps", "ra_d_GUPs")}
     if args.workload == "full" and not args.no_e2e:
-        if world > 1 and scaling == "weak":
+        if n_gpus > 1 and scaling == "weak":
             line["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": None,
                            "d2h_bytes_per_step": None,
                            "why": "weak-scaled global grid too large for per-rank host buffers"}
         else:
             line["e2e"] = e2e(ctx, sim, cfg, args, stream, world)
-            if world == 1:
+            if n_gpus == 1:
                 line["e2e_run"] = e2e_run(ctx, cfg, args, stream)
                 line["output_path"] = output_path(ctx, cfg, ms_per_step)
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and n_gpus == 1 and not args.no_cpu_baseline:
         rate, dt, kind, sample = cpu_reference_rate(grid, args.cpu_steps, args.workload)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": 1, "kind": kind,
                                 "sample": sample, "host_nproc": os.cpu_count()}

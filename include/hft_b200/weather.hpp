@@ -17,8 +17,16 @@
 // link the reference, hft::b200 also defines minimal look-alike types.
 //
 // Results are bitwise identical to the reference (see include/hftw.h).
-// Unlike the reference, device work can fail (no GPU, out of memory): the
-// adapter throws hft::b200::Error -- there is no CPU fallback.
+// Unlike the reference, device work can fail (no GPU, out of memory).  Each
+// entry point has two forms: the reference's signature, which throws
+// hft::b200::Error, and an overload taking the caller's Diagnostics& (the
+// reference's error convention, diagnostics.hpp:35-76) that never throws: it
+// reports diags.error({"<b200>", 0}, message, "b200-<code>") and returns
+// false.  There is no CPU fallback either way.
+//
+// Multi-GPU: a Placement runs the same calls on a px x py I x J decomposition
+// from this one host thread (hftw_create_multi; one device per rank, repeats
+// allowed), bitwise identical to one device.
 //------------------------------------------------------------------------------
 #pragma once
 
@@ -41,6 +49,52 @@ struct Error : std::runtime_error {
 inline void check(int rc, const hftw_ctx* ctx = nullptr) {
     if (rc != HFTW_OK) throw Error(rc, hftw_last_error(ctx));
 }
+
+/// Rule id of an hftw error code (Diagnostic::rule, diagnostics.hpp:26-31).
+inline const char* rule_of(int code) {
+    switch (code) {
+    case HFTW_EINVAL: return "b200-einval";
+    case HFTW_ECUDA: return "b200-ecuda";
+    case HFTW_ENOMEM: return "b200-enomem";
+    case HFTW_ESTATE: return "b200-estate";
+    case HFTW_EUNSUP: return "b200-eunsup";
+    }
+    return "b200-error";
+}
+
+/// Run `f`; an hft::b200::Error becomes diags.error({"<b200>", 0}, msg, rule).
+template <class Diags, class F>
+bool report_to(Diags& diags, F&& f) {
+    try {
+        f();
+        return true;
+    } catch (const Error& e) {
+        diags.error({"<b200>", 0}, e.what(), rule_of(e.code));
+    } catch (const std::exception& e) { // e.g. std::bad_alloc of a host SimState
+        diags.error({"<b200>", 0}, e.what(), "b200-host");
+    }
+    return false;
+}
+
+/// Where a simulation runs.  Default: one rank on `device`.  px x py > 1 (or a
+/// non-empty `devices`): that I x J decomposition in this process, rank r
+/// (= ry * px + rx) on devices[r], or on device r when `devices` is empty.
+struct Placement {
+    int device = 0;
+    int px = 1, py = 1;
+    std::vector<int> devices;
+    int layout = HFTW_IJK;
+
+    /// n GPUs 0..n-1 in the paper's process grids: 2 -> 2x1,
+    /// 4 -> 2x2, 8 -> 2x4; other n: n x 1.
+    static Placement gpus(int n) {
+        Placement p;
+        p.px = n == 4 ? 2 : n == 8 ? 2 : n;
+        p.py = n == 4 ? 2 : n == 8 ? 4 : 1;
+        return p;
+    }
+    bool multi() const { return px * py > 1 || !devices.empty(); }
+};
 
 // ---- minimal look-alike types (same member names as the reference) --------
 struct GridConfig {
@@ -118,6 +172,20 @@ public:
         : grid_(to_grid(cfg)) {
         check(hftw_create(&grid_, layout, device, &ctx_));
     }
+    /// On a Placement: one device, or a decomposition over several.
+    template <class Cfg>
+    Simulation(const Cfg& cfg, const Placement& where) : grid_(to_grid(cfg)) {
+        if (!where.multi()) {
+            check(hftw_create(&grid_, where.layout, where.device, &ctx_));
+            return;
+        }
+        const int n = where.px * where.py;
+        if (!where.devices.empty() && (int)where.devices.size() != n)
+            throw Error(HFTW_EINVAL, "Placement: one device per rank (" + std::to_string(n) +
+                                         "), got " + std::to_string(where.devices.size()));
+        check(hftw_create_multi(&grid_, where.layout, where.px, where.py,
+                                where.devices.empty() ? nullptr : where.devices.data(), &ctx_));
+    }
     Simulation(const Simulation&) = delete;
     Simulation& operator=(const Simulation&) = delete;
     ~Simulation() { hftw_destroy(ctx_); }
@@ -126,6 +194,9 @@ public:
     void step(long long n = 1) { check(hftw_step(ctx_, n), ctx_); }
     void sync() { check(hftw_sync(ctx_), ctx_); }
     void set_kernel(int k) { check(hftw_set_kernel(ctx_, k), ctx_); }
+    void set_option(int opt, long long v) { check(hftw_set_option(ctx_, opt, v), ctx_); }
+    /// Ranks this simulation runs on (1 unless placed on a decomposition).
+    int ranks() const { return hftw_group_size(ctx_); }
 
     template <class State>
     void upload(const State& st) {
@@ -163,6 +234,11 @@ void reference_init(const Cfg& cfg, State& st, int device = 0) {
     Simulation s(cfg, HFTW_IJK, device);
     s.init();
     s.download(st);
+}
+/// ... reporting failures to `diags` (no exceptions).
+template <class Cfg, class State, class Diags>
+bool reference_init(const Cfg& cfg, State& st, Diags& diags, int device = 0) {
+    return report_to(diags, [&] { reference_init(cfg, st, device); });
 }
 
 namespace detail {
@@ -239,15 +315,34 @@ void reference_step(const Cfg& cfg, State& st, int device = 0) {
           ctx);
 }
 
-/// hft::run_reference (weather.cpp:173-178).
+/// ... reporting failures to `diags` (no exceptions).
+template <class Cfg, class State, class Diags>
+bool reference_step(const Cfg& cfg, State& st, Diags& diags, int device = 0) {
+    return report_to(diags, [&] { reference_step(cfg, st, device); });
+}
+
+/// hft::run_reference (weather.cpp:173-178), on one device or on a Placement
+/// (e.g. run_reference(cfg, steps, Placement::gpus(8))).
 template <class State = SimState, class Cfg>
-State run_reference(const Cfg& cfg, long long steps, int device = 0) {
-    Simulation s(cfg, HFTW_IJK, device);
+State run_reference(const Cfg& cfg, long long steps, const Placement& where) {
+    Simulation s(cfg, where);
     s.init();
     s.step(steps);
     State st;
     s.download(st);
     return st;
+}
+template <class State = SimState, class Cfg>
+State run_reference(const Cfg& cfg, long long steps, int device = 0) {
+    Placement p;
+    p.device = device;
+    return run_reference<State>(cfg, steps, p);
+}
+/// ... into `out`, reporting failures to `diags` (no exceptions).
+template <class Cfg, class State, class Diags>
+bool run_reference(const Cfg& cfg, long long steps, State& out, Diags& diags,
+                   const Placement& where = {}) {
+    return report_to(diags, [&] { out = run_reference<State>(cfg, steps, where); });
 }
 
 } // namespace hft::b200

@@ -117,8 +117,10 @@ int hftw_step(hftw_ctx* ctx, int64_t nsteps);
  * the reference mutates its SimState); energy_u_out must not alias the inputs.
  * Equivalent to upload x3 + hftw_step(1) + download x2, but pipelined in
  * row blocks so that PCIe H2D, the step kernels and PCIe D2H overlap.
- * Synchronous; afterwards the context holds the stepped state.  Single-domain
- * contexts only. */
+ * Synchronous; afterwards the context holds the stepped state.  If it fails
+ * part-way, all copies have stopped when it returns and the device state is
+ * undefined: later calls fail with HFTW_ESTATE until hftw_init or an upload of
+ * all four fields.  A group context runs the same calls in sequence. */
 int hftw_step_host(hftw_ctx* ctx, const double* energy, const double* energy_surf,
                    const double* energy_pbl, double* energy_out, double* energy_u_out);
 
@@ -153,6 +155,17 @@ int hftw_set_kernel(hftw_ctx* ctx, int kernel);
 /* Kernel actually used by hftw_step (resolves AUTO). */
 int hftw_get_kernel(const hftw_ctx* ctx);
 
+/* Scheduling options of hftw_step (results are bitwise the same for every
+ * value; only the launch schedule changes).  The library reads no environment
+ * variables: kernel choice and tiling depend on the grid, the device and these
+ * calls only. */
+enum hftw_option {
+    HFTW_OPT_MULTISTEP = 1, /* single-step kernel, n >= 2 steps in ONE persistent launch:
+                               -1 never, 0 where a step is short (default), 1 always */
+    HFTW_OPT_PAIR = 2       /* AUTO may use two-step passes: 1 (default) or 0 */
+};
+int hftw_set_option(hftw_ctx* ctx, int option, int64_t value);
+
 /* Measurement hook: when on, every step launch is bracketed by CUDA events on
  * the context stream.  hftw_get_timing returns the summed device time (ms)
  * and the number of launches of one launch kind since timing was switched
@@ -186,7 +199,12 @@ double hftw_algorithmic_bytes(const hftw_ctx* ctx, int what);
 int hftw_launches_per_step(const hftw_ctx* ctx);
 
 /* Raw device view of a field for zero-copy interop: base pointer of logical
- * (i=0, j=0, k=1) and element strides (si, sj, sk); sk = 0 for 2D fields. */
+ * (i=0, j=0, k=1) and element strides (si, sj, sk); sk = 0 for 2D fields.
+ * The view is writable: any request first materialises ENERGY_U (so writes to
+ * ENERGY_SURF / ENERGY_PBL through a view cannot change it) and, for a
+ * decomposed rank, marks the halos stale (refilled by hftw_exchange).  The
+ * ENERGY and ENERGY_U pointers swap after every step (ping-pong store): take
+ * a fresh view after hftw_step. */
 int hftw_field_view(hftw_ctx* ctx, int field, void** dptr, int64_t strides[3]);
 
 /* ---- output path ----------------------------------
@@ -248,6 +266,28 @@ int hftw_peer_connect(hftw_ctx* ctx, const void* all, int world);
 int hftw_exchange(hftw_ctx* ctx);
 /* This rank's plan. */
 int hftw_get_plan(const hftw_ctx* ctx, hftw_plan* out);
+
+/* ---- multi-GPU from ONE host process ("multi-GPU fan-out is
+ * internal") ------------------------------------------------------------------
+ * A group context owns px*py rank subdomains, rank r on CUDA device
+ * devices[r] (devices == NULL: rank r on device r).  The ranks exchange halos
+ * exactly as above (in-kernel pushes + step flags) through plain device
+ * pointers: peer access is enabled between distinct devices (NVLink /
+ * NVSwitch); ranks that share a device run on one stream, one launch per step
+ * in rank order (that is how a single GPU can run -- and test -- any
+ * decomposition).  The handle works with every function of this header:
+ * init/upload/download take GLOBAL logical host arrays, hftw_step runs all
+ * ranks (halos are refilled automatically after init/upload), hftw_sync waits
+ * for every device.  Results are bitwise identical to the single-domain run.
+ * hftw_create_multi(grid, layout, 1, 1, devices, &ctx) is a one-rank group. */
+int hftw_create_multi(const hftw_grid* grid, int layout, int px, int py, const int* devices,
+                      hftw_ctx** out);
+/* Ranks of a group context (1 for any other context). */
+int hftw_group_size(const hftw_ctx* ctx);
+/* Rank r's own context (owned by the group: valid until hftw_destroy(group);
+ * for per-rank plans, timing and field views).  A plain context returns itself
+ * for r = 0. */
+int hftw_group_rank(hftw_ctx* ctx, int r, hftw_ctx** out);
 
 #ifdef __cplusplus
 }

@@ -79,13 +79,18 @@ def main():
 
     # (5) hashes at the BASELINE sizes (reference, full step)
     hashes = {}
-    for (nx, ny, nz, steps) in [(256, 256, 64, 10), (1581, 1301, 58, 2)]:
+    #     ASUCA x 20 / x 7: the default bench run and an odd count (pair passes
+    #     plus a single step); 3162x5204x58 x 5: BASELINE config 5's weak-scaling
+    #     grid (8 x ASUCA, ~31 GB of host memory here)
+    for (nx, ny, nz, steps) in [(256, 256, 64, 10), (1581, 1301, 58, 2), (1581, 1301, 58, 7),
+                                (1581, 1301, 58, 20), (3162, 5204, 58, 5)]:
         g = O.make_grid(nx, ny, nz)
         s = ref.run_reference(g, steps)
         hashes[f"{nx}x{ny}x{nz}_s{steps}"] = {
             "grid": grid_dict(g), "steps": steps, "source": "reference",
             "fnv1a64": {k: c.fnv(v) for k, v in s.fields().items()},
             "sum_energy": float(np.sum(s.energy))}
+        del s
         if nx == 256:
             # stencil-only config: diffusion of (init + 1 step) energy
             s1 = ref.run_reference(g, 1)

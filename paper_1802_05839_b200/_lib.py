@@ -18,6 +18,7 @@ FIELDS = {"energy": HFTW_ENERGY, "energy_u": HFTW_ENERGY_U,
 LAYOUTS = {"ijk": 0, "kij": 1}
 KERNELS = {"auto": 0, "fused_tma": 1, "fused_cell": 2, "split": 3, "fused_pair": 4}
 KERNEL_NAMES = {v: k for k, v in KERNELS.items()}
+OPTIONS = {"multistep": 1, "pair": 2}  # enum hftw_option
 ERRORS = {0: "ok", 1: "EINVAL", 2: "ECUDA", 3: "ENOMEM", 4: "ESTATE", 5: "EUNSUP"}
 
 
@@ -103,6 +104,11 @@ SIGNATURES = [
     ("hftw_peer_connect", C.c_int, [_P, _P, C.c_int]),
     ("hftw_exchange", C.c_int, [_P]),
     ("hftw_get_plan", C.c_int, [_P, C.POINTER(hftw_plan)]),
+    ("hftw_set_option", C.c_int, [_P, C.c_int, C.c_int64]),
+    ("hftw_create_multi", C.c_int, [C.POINTER(hftw_grid), C.c_int, C.c_int, C.c_int,
+                                    C.POINTER(C.c_int), C.POINTER(_P)]),
+    ("hftw_group_size", C.c_int, [_P]),
+    ("hftw_group_rank", C.c_int, [_P, C.c_int, C.POINTER(_P)]),
 ]
 
 # void (*)(void* user, const char* tag, double time, const double* field)

@@ -38,10 +38,18 @@ namespace {
 
 thread_local std::string g_err; // errors of calls without a context
 
-// Tuning knobs for experiments (HFTW_TX=32|64, HFTW_NS=stages, HFTW_CHUNK=rows).
+// Tuning knobs for the experiments under tools/ (HFTW_TX=32|64, HFTW_NS=stages,
+// HFTW_CHUNK=rows, ...): read ONLY in a -DHFTW_TUNING build (tools/build_variant.sh).
+// The default library ignores the environment, so kernel choice and tiling
+// depend on the grid, the device and the API (hftw_set_kernel/hftw_set_option).
 int env_int(const char* name, int dflt) {
+#ifdef HFTW_TUNING
     const char* v = std::getenv(name);
     return (v && *v) ? std::atoi(v) : dflt;
+#else
+    (void)name;
+    return dflt;
+#endif
 }
 
 constexpr int kFrontPad = 31; // IJK: logical i = 1 lands on a 256-byte boundary
@@ -117,7 +125,7 @@ struct hftw_ctx {
 
     // pair kernel (two steps per pass; single-domain IJK, nz <= 64)
     bool pair_ok = false;
-    bool pair_auto = env_int("HFTW_NO_PAIR", 0) == 0; // AUTO: two-step passes where available
+    bool pair_auto = env_int("HFTW_NO_PAIR", 0) == 0; // AUTO: two-step passes (HFTW_OPT_PAIR)
     int pair_ns = 0, pair_chunk = 0, pair_nchunks = 0, pair_ctas = 0;
     int pair_nbig = 0, pair_chunk2 = 0;
     bool pair_fast = false;     // every k-group has a compile-time row shape (AUTO uses it)
@@ -133,7 +141,8 @@ struct hftw_ctx {
     // multi-step wavefront launch (weather_wave.cuh): single-domain IJK
     bool wave_ok = false;
     int wave_chunk = 0, wave_nchunks = 0, wave_ctas = 0, wave_gtasks = 0;
-    bool wave_pref = false;     // multi-step launch preferred over one launch per step
+    bool wave_pref = false;     // multi-step launch preferred over one launch per step (auto)
+    int opt_multistep = 0;      // HFTW_OPT_MULTISTEP: -1 never, 0 auto (wave_pref), 1 always
     int* d_wave = nullptr;      // sched[2] + chunk_done[nchunks] + ghost_done[1]
 
     // measurement hook (hftw_set_timing)
@@ -171,6 +180,14 @@ struct hftw_ctx {
     double* host_stage[3] = {nullptr, nullptr, nullptr}; // dense logical energy in/out, energy_u
     void* flush_buf = nullptr;
     size_t flush_bytes = 0;
+
+    // a failed hftw_step_host leaves the device state undefined: the fields
+    // still to be re-uploaded (bit f = field f), cleared by init / uploads
+    unsigned poisoned = 0;
+
+    // group context (hftw_create_multi): one sub-context per rank in this process
+    std::vector<hftw_ctx*> ranks;
+    bool interleave = false; // ranks share a device: one launch per step, rank order
 
     std::string err;
 };
@@ -599,8 +616,7 @@ int launch_pair(hftw_ctx* c, int src) {
 // domain, IJK, same slab ring as the single-step kernel.
 int setup_wave(hftw_ctx* c) {
     c->wave_ok = false;
-    if (!c->tma_ok || c->layout != HFTW_IJK || c->tx != 64 || env_int("HFTW_NO_WAVE", 0))
-        return HFTW_OK;
+    if (!c->tma_ok || c->layout != HFTW_IJK || c->tx != 64) return HFTW_OK;
     auto kern = hftw::step_wave_kernel<64, kNCW>;
     CUDA_TRY(c, raise_smem_attr((const void*)kern, c->smem));
     int per_sm = 0;
@@ -635,11 +651,11 @@ int setup_wave(hftw_ctx* c) {
     // (6.9 units of 32 rows per CTA) separate launches run 0.383 ms/step against
     // 0.397 (less DRAM traffic: 1.05x vs 1.10x), while for the 1/4 and 1/8 ranks of a
     // 2x2 / 2x4 decomposition (1.8 and 1.0 units per CTA) the multi-step launch is
-    // 3% and 12% faster (tools/gpu_exp10.sh).  HFTW_WAVE=1 forces it (tests).
+    // 3% and 12% faster (tools/gpu_exp10.sh).  HFTW_OPT_MULTISTEP overrides it.
     {
         const long long slots = (long long)per_sm * c->num_sms;
         const long long units32 = (long long)c->nstrips * ((ny + 31) / 32);
-        c->wave_pref = env_int("HFTW_WAVE", 0) != 0 || units32 * 10 < slots * 27;
+        c->wave_pref = units32 * 10 < slots * 27;
     }
     c->wave_nchunks = (int)((ny + chunk - 1) / chunk);
     c->wave_gtasks = std::max(1, std::min(16, (int)((c->lnx + 2) * c->nz / 2048)));
@@ -809,6 +825,16 @@ int check_ctx(hftw_ctx* c) {
     return HFTW_OK;
 }
 
+// Calls that read the device state refuse it after a failed hftw_step_host.
+int check_state(hftw_ctx* c) {
+    if (c->poisoned)
+        return fail(c, HFTW_ESTATE, "device state undefined after a failed hftw_step_host: "
+                                    "call hftw_init or upload all four fields");
+    return HFTW_OK;
+}
+
+bool is_group(const hftw_ctx* c) { return c && !c->ranks.empty(); }
+
 // partition of n inner cells over p ranks (balanced; every rank >= 1 cell)
 long long part_lo(long long n, int p, int r) { return 1 + (long long)r * n / p; }
 long long part_hi(long long n, int p, int r) { return (long long)(r + 1) * n / p; }
@@ -950,6 +976,164 @@ int create_common(const hftw_grid* g, int layout, int device, const hftw_plan& p
     if ((rc = setup_pair(c))) return bail(rc);
     if ((rc = setup_wave(c))) return bail(rc);
     *out = c;
+    return HFTW_OK;
+}
+
+// ---- group contexts (hftw_create_multi): every rank in this process -------
+
+// Map the neighbours of rank c from the other ranks' device pointers (the
+// in-process counterpart of hftw_peer_connect's IPC mappings).
+void connect_local(hftw_ctx* c, const std::vector<hftw_ctx*>& ranks) {
+    for (int d = 0; d < 4; ++d) {
+        const int r = c->plan.nbr[d];
+        if (r < 0) {
+            c->peer[d] = PeerMap{};
+            continue;
+        }
+        const hftw_ctx* n = ranks[(size_t)r];
+        PeerMap m;
+        m.rank = r;
+        for (int b = 0; b < 2; ++b) m.buf[b] = n->buf[b] + n->off3;
+        m.sf = n->sf + n->off2;
+        m.pb = n->pb + n->off2;
+        m.flags = n->flags;
+        m.si = n->si;
+        m.sj = n->sj;
+        m.sk = n->sk;
+        m.s2j = n->s2j;
+        c->peer[d] = m;
+    }
+    c->connected = true;
+}
+
+int create_group(const hftw_grid* g, int layout, int px, int py, const int* devices,
+                 hftw_ctx** out) {
+    if (!out) return fail(nullptr, HFTW_EINVAL, "null output pointer");
+    *out = nullptr;
+    hftw_plan whole{};
+    int rc = make_plan(g, 1, 1, 0, &whole);
+    if (rc) return rc;
+    if (px < 1 || py < 1) return fail(nullptr, HFTW_EINVAL, "bad decomposition %dx%d", px, py);
+    const int n = px * py;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(nullptr, HFTW_ECUDA,
+                    "no CUDA device available (the B200 path has no CPU fallback)");
+    }
+    std::vector<int> dev((size_t)n);
+    for (int r = 0; r < n; ++r) {
+        dev[(size_t)r] = devices ? devices[r] : r;
+        if (dev[(size_t)r] < 0 || dev[(size_t)r] >= ndev)
+            return fail(nullptr, HFTW_EINVAL, "rank %d: bad device %d (%d visible)", r,
+                        dev[(size_t)r], ndev);
+    }
+    hftw_ctx* c = new hftw_ctx();
+    c->g = *g;
+    c->plan = whole;
+    c->plan.px = px;
+    c->plan.py = py;
+    c->plan.rank = -1;
+    c->layout = layout;
+    c->device = dev[0];
+    c->lnx = g->nx;
+    c->lny = g->ny;
+    c->nz = g->nz;
+    auto bail = [&](int code) {
+        hftw_destroy(c);
+        return code;
+    };
+    for (int r = 0; r < n; ++r) {
+        hftw_plan p{};
+        if ((rc = make_plan(g, px, py, r, &p))) return bail(rc);
+        hftw_ctx* sub = nullptr;
+        if ((rc = create_common(g, layout, dev[(size_t)r], p, n > 1, &sub))) {
+            const std::string why = g_err;
+            hftw_destroy(c);
+            return fail(nullptr, rc, "rank %d: %s", r, why.c_str());
+        }
+        c->ranks.push_back(sub);
+    }
+    // Ranks on one device share its stream and run one launch per step in rank
+    // order: every launch of step s then finds its neighbours' step s-1
+    // complete, so no kernel ever waits on a kernel queued behind it.
+    for (int r = 1; r < n; ++r)
+        for (int q = 0; q < r; ++q)
+            if (dev[(size_t)q] == dev[(size_t)r]) {
+                hftw_ctx* sub = c->ranks[(size_t)r];
+                cudaSetDevice(sub->device);
+                if (sub->own_stream) cudaStreamDestroy(sub->stream);
+                sub->stream = c->ranks[(size_t)q]->stream;
+                sub->own_stream = false;
+                c->interleave = true;
+                break;
+            }
+    // peer access between neighbouring ranks on distinct devices (NVLink)
+    for (int r = 0; r < n; ++r)
+        for (int d = 0; d < 4; ++d) {
+            const int q = c->ranks[(size_t)r]->plan.nbr[d];
+            if (q < 0 || dev[(size_t)q] == dev[(size_t)r]) continue;
+            int can = 0;
+            cudaDeviceCanAccessPeer(&can, dev[(size_t)r], dev[(size_t)q]);
+            if (!can)
+                return bail(fail(nullptr, HFTW_EUNSUP, "device %d cannot access device %d",
+                                 dev[(size_t)r], dev[(size_t)q]));
+            cudaSetDevice(dev[(size_t)r]);
+            const cudaError_t e = cudaDeviceEnablePeerAccess(dev[(size_t)q], 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+            else if (e != cudaSuccess)
+                return bail(fail(nullptr, HFTW_ECUDA, "cudaDeviceEnablePeerAccess(%d -> %d): %s",
+                                 dev[(size_t)r], dev[(size_t)q], cudaGetErrorString(e)));
+        }
+    for (hftw_ctx* sub : c->ranks) {
+        connect_local(sub, c->ranks);
+        sub->halo_dirty = sub->dist;
+    }
+    c->stream = c->ranks[0]->stream;
+    c->own_stream = false;
+    c->tma_ok = c->ranks[0]->tma_ok;
+    c->pair_ok = c->ranks[0]->pair_ok;
+    *out = c;
+    return HFTW_OK;
+}
+
+// A rank's failure, reported on the group.
+int rank_fail(hftw_ctx* c, const hftw_ctx* r, int rc) {
+    if (!rc) return HFTW_OK;
+    return fail(c, rc, "rank %d: %s", r->plan.rank, r->err.c_str());
+}
+
+#define RANK_TRY(c, r, x)                                                                      \
+    do {                                                                                       \
+        const int rc_ = (x);                                                                   \
+        if (rc_) return rank_fail((c), (r), rc_);                                              \
+    } while (0)
+
+// Refill every rank's halos (after init / upload / physics): all devices idle,
+// then each rank pushes its faces and resets its step flags.
+int group_exchange(hftw_ctx* c) {
+    for (hftw_ctx* r : c->ranks) RANK_TRY(c, r, hftw_sync(r));
+    for (hftw_ctx* r : c->ranks) RANK_TRY(c, r, hftw_exchange(r));
+    return HFTW_OK;
+}
+
+int group_step(hftw_ctx* c, int64_t nsteps) {
+    if (nsteps < 0) return fail(c, HFTW_EINVAL, "steps must be nonnegative");
+    if (nsteps == 0) return HFTW_OK;
+    for (hftw_ctx* r : c->ranks)
+        if (r->halo_dirty) {
+            int rc = group_exchange(c);
+            if (rc) return rc;
+            break;
+        }
+    if (c->interleave) {
+        for (int64_t s = 0; s < nsteps; ++s)
+            for (hftw_ctx* r : c->ranks) RANK_TRY(c, r, hftw_step(r, 1));
+    } else {
+        // distinct devices: each rank queues all its steps on its own stream;
+        // the kernels order themselves through the step flags
+        for (hftw_ctx* r : c->ranks) RANK_TRY(c, r, hftw_step(r, nsteps));
+    }
     return HFTW_OK;
 }
 
@@ -1098,6 +1282,29 @@ int hftw_create(const hftw_grid* g, int layout, int device, hftw_ctx** out) {
     return create_common(g, layout, device, p, false, out);
 }
 
+int hftw_create_multi(const hftw_grid* g, int layout, int px, int py, const int* devices,
+                      hftw_ctx** out) {
+    if (!g) return fail(nullptr, HFTW_EINVAL, "null grid");
+    char msg[512];
+    if (hftw_validate(g, msg, sizeof msg) != HFTW_OK) return fail(nullptr, HFTW_EINVAL, "%s", msg);
+    if (layout != HFTW_IJK && layout != HFTW_KIJ)
+        return fail(nullptr, HFTW_EINVAL, "unknown layout %d", layout);
+    return create_group(g, layout, px, py, devices, out);
+}
+
+int hftw_group_size(const hftw_ctx* c) {
+    if (!c) return 0;
+    return is_group(c) ? (int)c->ranks.size() : 1;
+}
+
+int hftw_group_rank(hftw_ctx* c, int r, hftw_ctx** out) {
+    if (!c || !out) return fail(nullptr, HFTW_EINVAL, "null argument");
+    const int n = hftw_group_size(c);
+    if (r < 0 || r >= n) return fail(c, HFTW_EINVAL, "rank %d of %d", r, n);
+    *out = is_group(c) ? c->ranks[(size_t)r] : c;
+    return HFTW_OK;
+}
+
 int hftw_create_dist(const hftw_grid* g, int layout, int device, int px, int py, int rank,
                      hftw_ctx** out) {
     if (!g) return fail(nullptr, HFTW_EINVAL, "null grid");
@@ -1111,6 +1318,13 @@ int hftw_create_dist(const hftw_grid* g, int layout, int device, int px, int py,
 
 void hftw_destroy(hftw_ctx* c) {
     if (!c) return;
+    if (is_group(c)) {
+        // reverse order: a stream shared by ranks of one device belongs to the
+        // lowest of them
+        for (size_t r = c->ranks.size(); r-- > 0;) hftw_destroy(c->ranks[r]);
+        delete c;
+        return;
+    }
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     for (void* p : c->ipc_opened) cudaIpcCloseMemHandle(p);
@@ -1148,6 +1362,10 @@ void hftw_destroy(hftw_ctx* c) {
 int hftw_init(hftw_ctx* c) {
     int rc = check_ctx(c);
     if (rc) return rc;
+    if (is_group(c)) {
+        for (hftw_ctx* r : c->ranks) RANK_TRY(c, r, hftw_init(r));
+        return HFTW_OK;
+    }
     for (int b = 0; b < 2; ++b)
         CUDA_TRY(c, cudaMemsetAsync(c->buf[b], 0, c->n3 * sizeof(double), c->stream));
     Dom d = make_dom(c);
@@ -1166,6 +1384,7 @@ int hftw_init(hftw_ctx* c) {
     if (c->d_sched) CUDA_TRY(c, cudaMemsetAsync(c->d_sched, 0, 2 * sizeof(int), c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     c->eu_derived = false; // energy_u is all zeros (weather.cpp:82)
+    c->poisoned = 0;
     if (c->dist) c->halo_dirty = true;
     return HFTW_OK;
 }
@@ -1175,6 +1394,10 @@ int hftw_upload(hftw_ctx* c, int field, const double* host) {
     if (rc) return rc;
     if (!valid_field(field) || !host)
         return fail(c, HFTW_EINVAL, "bad field %d or null buffer", field);
+    if (is_group(c)) {
+        for (hftw_ctx* r : c->ranks) RANK_TRY(c, r, hftw_upload(r, field, host));
+        return HFTW_OK;
+    }
     double* h = const_cast<double*>(host);
     switch (field) {
     case HFTW_ENERGY:
@@ -1187,12 +1410,13 @@ int hftw_upload(hftw_ctx* c, int field, const double* host) {
     case HFTW_ENERGY_SURF:
     case HFTW_ENERGY_PBL:
         // a derived energy_u depends on the boundary fields of its step
-        if ((rc = materialize_eu(c))) return rc;
+        if (!c->poisoned && (rc = materialize_eu(c))) return rc;
         rc = copy_2d(c, field == HFTW_ENERGY_SURF ? sf2(c) : pb2(c), h, true);
         break;
     }
     if (rc) return rc;
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    c->poisoned &= ~(1u << field);
     if (c->dist && field != HFTW_ENERGY_U) c->halo_dirty = true;
     return HFTW_OK;
 }
@@ -1202,6 +1426,11 @@ int hftw_download(hftw_ctx* c, int field, double* host) {
     if (rc) return rc;
     if (!valid_field(field) || !host)
         return fail(c, HFTW_EINVAL, "bad field %d or null buffer", field);
+    if (is_group(c)) {
+        for (hftw_ctx* r : c->ranks) RANK_TRY(c, r, hftw_download(r, field, host));
+        return HFTW_OK;
+    }
+    if ((rc = check_state(c))) return rc;
     switch (field) {
     case HFTW_ENERGY:
         rc = copy_3d(c, e3(c, c->cur), host, false);
@@ -1225,6 +1454,8 @@ int hftw_download(hftw_ctx* c, int field, double* host) {
 int hftw_step(hftw_ctx* c, int64_t nsteps) {
     int rc = check_ctx(c);
     if (rc) return rc;
+    if (is_group(c)) return group_step(c, nsteps);
+    if ((rc = check_state(c))) return rc;
     if (nsteps < 0) return fail(c, HFTW_EINVAL, "steps must be nonnegative");
     if (nsteps == 0) return HFTW_OK;
     const int k = resolved_kernel(c);
@@ -1249,8 +1480,9 @@ int hftw_step(hftw_ctx* c, int64_t nsteps) {
         }
         nsteps -= 2 * pairs;
     }
-    if ((k == HFTW_KERNEL_FUSED_TMA || k == HFTW_KERNEL_FUSED_PAIR) && c->wave_ok &&
-        c->wave_pref && nsteps >= 2 && c->tma_ok) {
+    const bool multistep = c->opt_multistep > 0 || (c->opt_multistep == 0 && c->wave_pref);
+    if ((k == HFTW_KERNEL_FUSED_TMA || k == HFTW_KERNEL_FUSED_PAIR) && c->wave_ok && multistep &&
+        nsteps >= 2 && c->tma_ok) {
         // all steps in one persistent launch (weather_wave.cuh); chunks of
         // at most 2^20 steps keep the work-list index in an int (decomposed:
         // kMaxWaveStepsDist, the per-step completion counters)
@@ -1292,6 +1524,10 @@ int hftw_step(hftw_ctx* c, int64_t nsteps) {
 int hftw_set_timing(hftw_ctx* c, int on) {
     int rc = check_ctx(c);
     if (rc) return rc;
+    if (is_group(c)) {
+        for (hftw_ctx* r : c->ranks) RANK_TRY(c, r, hftw_set_timing(r, on));
+        return HFTW_OK;
+    }
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     for (auto& t : c->tev) {
         cudaEventDestroy(t.a);
@@ -1306,6 +1542,16 @@ int hftw_get_timing(hftw_ctx* c, int kind, double* ms, int64_t* launches, int64_
     int rc = check_ctx(c);
     if (rc) return rc;
     if (!ms || !launches) return fail(c, HFTW_EINVAL, "null output");
+    if (is_group(c)) {
+        // launches and steps of rank 0; the device time of the slowest rank
+        double worst = 0.0;
+        for (size_t r = c->ranks.size(); r-- > 0;) {
+            RANK_TRY(c, c->ranks[r], hftw_get_timing(c->ranks[r], kind, ms, launches, steps));
+            worst = std::max(worst, *ms);
+        }
+        *ms = worst;
+        return HFTW_OK;
+    }
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     double tot = 0.0;
     int64_t n = 0, st = 0;
@@ -1326,6 +1572,10 @@ int hftw_get_timing(hftw_ctx* c, int kind, double* ms, int64_t* launches, int64_
 int hftw_sync(hftw_ctx* c) {
     int rc = check_ctx(c);
     if (rc) return rc;
+    if (is_group(c)) {
+        for (hftw_ctx* r : c->ranks) RANK_TRY(c, r, hftw_sync(r));
+        return HFTW_OK;
+    }
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     return HFTW_OK;
 }
@@ -1354,6 +1604,7 @@ int hftw_run_reference(const hftw_grid* g, int64_t steps, int device, double* e,
 int hftw_set_stream(hftw_ctx* c, void* s) {
     int rc = check_ctx(c);
     if (rc) return rc;
+    if (is_group(c)) return fail(c, HFTW_EUNSUP, "a group context keeps one stream per device");
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     if (c->own_stream) cudaStreamDestroy(c->stream);
     if (s) {
@@ -1370,6 +1621,10 @@ void* hftw_stream(hftw_ctx* c) { return c ? static_cast<void*>(c->stream) : null
 
 int hftw_set_kernel(hftw_ctx* c, int k) {
     if (!c) return fail(nullptr, HFTW_EINVAL, "null context");
+    if (is_group(c)) {
+        for (hftw_ctx* r : c->ranks) RANK_TRY(c, r, hftw_set_kernel(r, k));
+        return HFTW_OK;
+    }
     if (k < HFTW_KERNEL_AUTO || k > HFTW_KERNEL_FUSED_PAIR)
         return fail(c, HFTW_EINVAL, "bad kernel %d", k);
     if (k == HFTW_KERNEL_FUSED_PAIR && !c->pair_ok)
@@ -1381,12 +1636,39 @@ int hftw_set_kernel(hftw_ctx* c, int k) {
     return HFTW_OK;
 }
 
-int hftw_get_kernel(const hftw_ctx* c) { return c ? resolved_kernel(c) : -1; }
+int hftw_get_kernel(const hftw_ctx* c) {
+    if (is_group(c)) return hftw_get_kernel(c->ranks[0]);
+    return c ? resolved_kernel(c) : -1;
+}
+
+int hftw_set_option(hftw_ctx* c, int opt, int64_t v) {
+    if (!c) return fail(nullptr, HFTW_EINVAL, "null context");
+    if (is_group(c)) {
+        for (hftw_ctx* r : c->ranks) RANK_TRY(c, r, hftw_set_option(r, opt, v));
+        return HFTW_OK;
+    }
+    switch (opt) {
+    case HFTW_OPT_MULTISTEP:
+        if (v < -1 || v > 1) return fail(c, HFTW_EINVAL, "HFTW_OPT_MULTISTEP takes -1, 0 or 1");
+        c->opt_multistep = (int)v;
+        return HFTW_OK;
+    case HFTW_OPT_PAIR:
+        if (v != 0 && v != 1) return fail(c, HFTW_EINVAL, "HFTW_OPT_PAIR takes 0 or 1");
+        c->pair_auto = v != 0;
+        return HFTW_OK;
+    }
+    return fail(c, HFTW_EINVAL, "unknown option %d", opt);
+}
 
 int hftw_physics(hftw_ctx* c, int mode) {
     int rc = check_ctx(c);
     if (rc) return rc;
     if (mode != 0 && mode != 1) return fail(c, HFTW_EINVAL, "bad physics mode %d", mode);
+    if (is_group(c)) {
+        for (hftw_ctx* r : c->ranks) RANK_TRY(c, r, hftw_physics(r, mode));
+        return HFTW_OK;
+    }
+    if ((rc = check_state(c))) return rc;
     if ((rc = materialize_eu(c))) return rc;
     if ((rc = launch_physics(c, c->cur, mode))) return rc;
     if (c->dist) c->halo_dirty = true;
@@ -1396,7 +1678,9 @@ int hftw_physics(hftw_ctx* c, int mode) {
 int hftw_diffuse(hftw_ctx* c) {
     int rc = check_ctx(c);
     if (rc) return rc;
-    if (c->dist) return fail(c, HFTW_EUNSUP, "diffusion-only sweeps are single-domain");
+    if (c->dist || is_group(c))
+        return fail(c, HFTW_EUNSUP, "diffusion-only sweeps are single-domain");
+    if ((rc = check_state(c))) return rc;
     if ((rc = launch_fused<false>(c, c->cur,
                                   c->tma_ok ? HFTW_KERNEL_FUSED_TMA : HFTW_KERNEL_FUSED_CELL)))
         return rc;
@@ -1407,6 +1691,11 @@ int hftw_diffuse(hftw_ctx* c) {
 
 double hftw_algorithmic_bytes(const hftw_ctx* c, int what) {
     if (!c) return 0.0;
+    if (is_group(c)) {
+        double t = 0.0;
+        for (const hftw_ctx* r : c->ranks) t += hftw_algorithmic_bytes(r, what);
+        return t;
+    }
     // this context's stored cells (its subdomain's owned cells when decomposed)
     const Box o = owned_box(c);
     const double cols = (double)(o.i1 - o.i0 + 1) * (double)(o.j1 - o.j0 + 1);
@@ -1421,6 +1710,7 @@ double hftw_algorithmic_bytes(const hftw_ctx* c, int what) {
 
 int hftw_launches_per_step(const hftw_ctx* c) {
     if (!c) return 0;
+    if (is_group(c)) return hftw_launches_per_step(c->ranks[0]) * (int)c->ranks.size();
     return resolved_kernel(c) == HFTW_KERNEL_SPLIT ? 2 : 1;
 }
 
@@ -1428,7 +1718,14 @@ int hftw_field_view(hftw_ctx* c, int field, void** dptr, int64_t strides[3]) {
     int rc = check_ctx(c);
     if (rc) return rc;
     if (!valid_field(field) || !dptr || !strides) return fail(c, HFTW_EINVAL, "bad arguments");
-    if (field == HFTW_ENERGY_U && (rc = materialize_eu(c))) return rc;
+    if (is_group(c))
+        return fail(c, HFTW_EUNSUP, "a group has one view per rank (hftw_group_rank)");
+    if ((rc = check_state(c))) return rc;
+    // the view is writable: energy_u must not depend on sf/pb any more, and a
+    // decomposed rank's halos must be refilled before the next step
+    if ((rc = materialize_eu(c))) return rc;
+    CUDA_TRY(c, cudaStreamSynchronize(c->stream));
+    if (c->dist) c->halo_dirty = true;
     switch (field) {
     case HFTW_ENERGY: *dptr = e3(c, c->cur); break;
     case HFTW_ENERGY_U: *dptr = e3(c, c->cur ^ 1); break;
@@ -1445,6 +1742,7 @@ int hftw_field_view(hftw_ctx* c, int field, void** dptr, int64_t strides[3]) {
 int hftw_flush_l2(hftw_ctx* c, size_t bytes) {
     int rc = check_ctx(c);
     if (rc) return rc;
+    if (is_group(c)) return rank_fail(c, c->ranks[0], hftw_flush_l2(c->ranks[0], bytes));
     bytes = (bytes + 31) / 32 * 32;
     if (c->flush_bytes < bytes) {
         if (c->flush_buf) cudaFree(c->flush_buf);
@@ -1465,6 +1763,7 @@ size_t hftw_peer_desc_size(void) { return sizeof(PeerDesc); }
 int hftw_peer_export(hftw_ctx* c, void* out) {
     int rc = check_ctx(c);
     if (rc) return rc;
+    if (is_group(c)) return fail(c, HFTW_EUNSUP, "a group connects its ranks itself");
     if (!out) return fail(c, HFTW_EINVAL, "null descriptor buffer");
     PeerDesc pd{};
     for (int b = 0; b < 2; ++b) CUDA_TRY(c, cudaIpcGetMemHandle(&pd.buf[b], c->buf[b]));
@@ -1486,6 +1785,7 @@ int hftw_peer_export(hftw_ctx* c, void* out) {
 int hftw_peer_connect(hftw_ctx* c, const void* all, int world) {
     int rc = check_ctx(c);
     if (rc) return rc;
+    if (is_group(c)) return fail(c, HFTW_EUNSUP, "a group connects its ranks itself");
     if (!all || world != c->plan.px * c->plan.py)
         return fail(c, HFTW_EINVAL, "need %d descriptors, got %d", c->plan.px * c->plan.py, world);
     const PeerDesc* pds = static_cast<const PeerDesc*>(all);
@@ -1531,6 +1831,8 @@ int hftw_peer_connect(hftw_ctx* c, const void* all, int world) {
 int hftw_exchange(hftw_ctx* c) {
     int rc = check_ctx(c);
     if (rc) return rc;
+    if (is_group(c)) return group_exchange(c);
+    if ((rc = check_state(c))) return rc;
     if (!c->dist) {
         c->halo_dirty = false;
         return HFTW_OK;
@@ -1569,6 +1871,51 @@ static double modulo_real(double a, double p) {
     return a - m;
 }
 
+} // extern "C"
+
+namespace {
+// hftw_simulate on a group context: the same time loop, each output gathered
+// from the ranks synchronously into one pinned logical buffer.
+int group_simulate(hftw_ctx* c, double start_time, double end_time, double timestep,
+                   double output_timestep, hftw_write_fn write, void* user, int64_t* steps_done,
+                   int64_t* writes_done) {
+    const size_t n = (size_t)((c->g.nx + 2) * (c->g.ny + 2) * c->g.nz);
+    double* host = nullptr;
+    if (write) CUDA_TRY(c, cudaMallocHost(&host, n * sizeof(double)));
+    auto due = [&](double t) {
+        volatile double pr = t + 0.001;
+        return write && modulo_real(pr, output_timestep) < 0.01;
+    };
+    int rc = HFTW_OK;
+    int64_t steps = 0, writes = 0;
+    double time = start_time;
+    for (;;) {
+        if (due(time)) {
+            if ((rc = hftw_download(c, HFTW_ENERGY, host))) break;
+            write(user, "energy", time, host);
+            ++writes;
+        }
+        int64_t k = 0;
+        double t = time;
+        do {
+            ++k;
+            t = t + timestep;
+        } while (!(t > end_time) && !due(t));
+        if ((rc = hftw_step(c, k))) break;
+        steps += k;
+        time = t;
+        if (time > end_time) break;
+    }
+    if (host) cudaFreeHost(host);
+    if (rc) return rc;
+    if (steps_done) *steps_done = steps;
+    if (writes_done) *writes_done = writes;
+    return HFTW_OK;
+}
+} // namespace
+
+extern "C" {
+
 int hftw_simulate(hftw_ctx* c, double start_time, double end_time, double timestep,
                   double output_timestep, hftw_write_fn write, void* user, int64_t* steps_done,
                   int64_t* writes_done) {
@@ -1577,6 +1924,10 @@ int hftw_simulate(hftw_ctx* c, double start_time, double end_time, double timest
     if (c->dist) return fail(c, HFTW_EUNSUP, "hftw_simulate runs on single-domain contexts");
     if (!(timestep > 0.0) || !(output_timestep > 0.0))
         return fail(c, HFTW_EINVAL, "timestep and output timestep must be positive");
+    if (is_group(c))
+        return group_simulate(c, start_time, end_time, timestep, output_timestep, write, user,
+                              steps_done, writes_done);
+    if ((rc = check_state(c))) return rc;
     const long long nx = c->g.nx, ny = c->g.ny, nz = c->g.nz;
     const size_t n = (size_t)((nx + 2) * (ny + 2) * nz);
     if (write && c->out.empty()) {
@@ -1689,6 +2040,15 @@ int hftw_host_unregister(void* ptr) {
     return HFTW_OK;
 }
 
+} // extern "C"
+
+namespace {
+int step_host_pipeline(hftw_ctx* c, const double* energy, const double* energy_surf,
+                       const double* energy_pbl, double* energy_out, double* energy_u_out);
+}
+
+extern "C" {
+
 int hftw_step_host(hftw_ctx* c, const double* energy, const double* energy_surf,
                    const double* energy_pbl, double* energy_out, double* energy_u_out) {
     int rc = check_ctx(c);
@@ -1697,9 +2057,8 @@ int hftw_step_host(hftw_ctx* c, const double* energy, const double* energy_surf,
         return fail(c, HFTW_EINVAL, "null host buffer");
     if (c->dist)
         return fail(c, HFTW_EUNSUP, "hftw_step_host runs on single-domain contexts");
-    double* e_in = const_cast<double*>(energy);
     const int rk = resolved_kernel(c);
-    if (!c->tma_ok || c->layout != HFTW_IJK ||
+    if (is_group(c) || !c->tma_ok || c->layout != HFTW_IJK ||
         (rk != HFTW_KERNEL_FUSED_TMA && rk != HFTW_KERNEL_FUSED_PAIR)) {
         // no row-block pipeline for this configuration: the same calls in sequence
         if ((rc = hftw_upload(c, HFTW_ENERGY, energy)) ||
@@ -1710,6 +2069,27 @@ int hftw_step_host(hftw_ctx* c, const double* energy, const double* energy_surf,
             return rc;
         return HFTW_OK;
     }
+    rc = step_host_pipeline(c, energy, energy_surf, energy_pbl, energy_out, energy_u_out);
+    if (rc) {
+        // stop every copy into / out of the caller's buffers before returning;
+        // the device state (partly scattered input, new sf/pb) is now undefined
+        if (c->h2d_stream) cudaStreamSynchronize(c->h2d_stream);
+        if (c->d2h_stream) cudaStreamSynchronize(c->d2h_stream);
+        cudaStreamSynchronize(c->stream);
+        cudaGetLastError();
+        c->eu_derived = false;
+        c->poisoned = 0xF;
+    }
+    return rc;
+}
+
+} // extern "C"
+
+namespace {
+int step_host_pipeline(hftw_ctx* c, const double* energy, const double* energy_surf,
+                       const double* energy_pbl, double* energy_out, double* energy_u_out) {
+    int rc = HFTW_OK;
+    double* e_in = const_cast<double*>(energy);
     // Row blocks of whole TMA chunks.  Block b: ONE 2D H2D copy of its rows
     // (all k) into a dense staging copy of the host array (h2d stream); on the
     // compute stream, scatter into the padded field and -- once block b+1 has
@@ -1756,12 +2136,8 @@ int hftw_step_host(hftw_ctx* c, const double* energy, const double* energy_surf,
         return b == nb - 1 ? ny + 1 : std::min<long long>(ny, (long long)chunk_lo(b + 1) * c->chunk);
     };
     // rows [r0, r1] of all k: nz runs of (nx+2)(r1-r0+1) doubles, one plane apart
-    const int skip = env_int("HFTW_PIPE_SKIP", 0); // tools/e2e_probe.py only: 1 = no H2D, 2 = no D2H
     auto pcie = [&](double* dst, const double* srcp, long long r0, long long r1,
                     cudaMemcpyKind kind, cudaStream_t st) -> int {
-        if ((skip == 1 && kind == cudaMemcpyHostToDevice) ||
-            (skip == 2 && kind == cudaMemcpyDeviceToHost))
-            return HFTW_OK;
         const size_t pitch = (size_t)hsk * 8, width = (size_t)(hsj * (r1 - r0 + 1)) * 8;
         CUDA_TRY(c, cudaMemcpy2DAsync(dst + r0 * hsj, pitch, srcp + r0 * hsj, pitch, width,
                                       (size_t)nz, kind, st));
@@ -1831,13 +2207,17 @@ int hftw_step_host(hftw_ctx* c, const double* energy, const double* energy_surf,
     // the context now holds the stepped state, as after upload x3 + step(1)
     c->cur ^= 1;
     c->eu_derived = true;
+    c->poisoned = 0;
     ++c->step_count;
     return HFTW_OK;
 }
+} // namespace
+
+extern "C" {
 
 int hftw_get_plan(const hftw_ctx* c, hftw_plan* out) {
     if (!c || !out) return fail(nullptr, HFTW_EINVAL, "null argument");
-    *out = c->plan;
+    *out = c->plan; // a group: px x py of the whole grid, rank -1
     return HFTW_OK;
 }
 

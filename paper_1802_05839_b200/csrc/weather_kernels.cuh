@@ -151,12 +151,29 @@ __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned l
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// Spin-wait watchdog: a flag wait that cannot end (a neighbour rank died or
+// was never launched) traps after kSpinLimitNs, so the launch fails with an
+// error instead of hanging the device.
+constexpr unsigned long long kSpinLimitNs = 20ull * 1000ull * 1000ull * 1000ull;
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void spin_check(unsigned long long t0) {
+    if (globaltimer_ns() - t0 > kSpinLimitNs) __trap();
+}
+
 // Wait until every neighbour in `mask` (bit d = hftw_dir d) finished step-1.
 __device__ __forceinline__ void halo_wait(const Halo& h, int mask) {
     if (!h.active) return;
     for (int d = 0; d < 4; ++d) {
         if (!((mask >> d) & 1) || !h.nb[d]) continue;
-        while ((long long)ld_acquire_sys(&h.my_flags[d]) < h.step) __nanosleep(64);
+        const unsigned long long t0 = globaltimer_ns();
+        while ((long long)ld_acquire_sys(&h.my_flags[d]) < h.step) {
+            __nanosleep(64);
+            spin_check(t0);
+        }
     }
 }
 
@@ -312,7 +329,7 @@ __global__ void __launch_bounds__(256) physics_rows_kernel(double* __restrict__ 
                                                            const double* __restrict__ pb,
                                                            Dom d) {
     Owned o = owned(d);
-    const int ni = o.i1 - o.i0 + 1, nj = o.j1 - o.j0 + 1;
+    const int nj = o.j1 - o.j0 + 1;
     const long long rows = (long long)nj * d.nz;
     for (long long r = blockIdx.x; r < rows; r += gridDim.x) {
         const int j = o.j0 + (int)(r % nj), k = 1 + (int)(r / nj);
@@ -714,15 +731,8 @@ __device__ __forceinline__ void column_row(const ColumnRow& r, const Halo& h, co
             s6 = dadd(s6, pin<PHYS>(pm[0], ri));
             s6 = dadd(s6, pin<PHYS>(pp[0], ri));
             s6 = dadd(dadd(s6, pd), pn);
-            double out = dadd(dmul(c6, pc), dmul(dv, s6));
-#if defined(HFTW_EXPERIMENT_COPY_ONLY) // tools/ experiment: memory path alone
-            out = p0[0];
-#endif
-#if !defined(HFTW_EXPERIMENT_NO_STORE)
+            const double out = dadd(dmul(c6, pc), dmul(dv, s6));
             *q = out;
-#else
-            if (out == -12345.678) *q = out; // keep the math live
-#endif
             if (PUSH) halo_push(h, d, r.i, r.j, k, out);
             q += r.sk;
             p0 += w;
@@ -757,7 +767,6 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     uint64_t* empty = full + NS;
     int* slot_unit = reinterpret_cast<int*>(empty + NS); // work unit of each staged slab
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int units = a.u_hi - a.u_lo;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < NS; ++s) {
@@ -844,7 +853,9 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
             const uint32_t slot = L % NS;
             mbar_wait(&full[slot], (L / NS) & 1);
         }
-        const int unit = slot_unit[L % NS];
+        int unit = 0; // one reader per warp (see weather_wave.cuh)
+        if (lane == 0) unit = slot_unit[L % NS];
+        unit = __shfl_sync(0xffffffffu, unit, 0);
         if (unit < 0) break;
         const int ch = unit / a.nstrips, st = unit % a.nstrips;
         const int ja = ch * a.chunk + 1, jb = min(d.ny, ja + a.chunk - 1);

@@ -45,21 +45,15 @@ namespace hftw {
 #endif
 constexpr int kPairTX = HFTW_PAIR_TX;           // output columns per strip (30: 2 CTAs per SM)
 constexpr int kPairIC = kPairTX + 2;            // intermediate columns i0-1 .. i0+TX (warps)
-constexpr int kPairW = kPairTX + 4;             // slab columns i0-2 .. i0+63
+constexpr int kPairW = kPairTX + 4;             // slab columns i0-2 .. i0+TX+1
 #ifndef HFTW_PAIR_KG
 #define HFTW_PAIR_KG 8
 #endif
 constexpr int kPairKG = HFTW_PAIR_KG;           // k-groups (8: 512 threads, <= 8 planes each)
 constexpr int kPairThreads = kPairIC * kPairKG;
 constexpr int kPairMinBlocks = kPairThreads <= 256 ? 2 : 1; // CTAs per SM the tile allows
-#ifndef HFTW_PAIR_NIB
-#define HFTW_PAIR_NIB 3
-#endif
 // intermediate row buffers (rows j-1, j, j+1), one CTA barrier per row
-#ifndef HFTW_PAIR_BAR2
-#define HFTW_PAIR_BAR2 0 // 1: the earlier second barrier per row (A/B measurement only)
-#endif
-constexpr int kPairNIB = HFTW_PAIR_NIB;
+constexpr int kPairNIB = 3;
 
 __host__ __device__ inline int round128(int b) { return (b + 127) / 128 * 128; }
 
@@ -375,7 +369,7 @@ __device__ __forceinline__ void pair_ghost_cols(const Dom& d, const PairArgs& a,
 }
 
 // The second producer of a strip's j-ghost intermediates computes that
-// strip's j-ghost cells (i in i0..i0+61 clipped to 1..nx, j = 0 and ny+1):
+// strip's j-ghost cells (i in i0..i0+TX-1 clipped to 1..nx, j = 0 and ny+1):
 // weather.cpp:155-158 on the intermediate field.
 __device__ __forceinline__ void pair_ghost_rows(const Dom& d, const PairArgs& a,
                                              double* __restrict__ u, int i0, int tid) {
@@ -484,7 +478,7 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
     }
     __syncthreads();
 
-    // thread -> (intermediate column cc = 1 .. 64 = logical i0-2+cc, k-group g)
+    // thread -> (intermediate column cc = 1 .. TX+2 = logical i0-2+cc, k-group g)
     const int cc = 1 + (tid % kPairIC);
     const int g = tid / kPairIC;
     // k-groups: planes kl .. kh, nk = kh - kl + 1 <= KPT.  The first and last
@@ -607,9 +601,6 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
             // as Bm, at this thread's own column and planes; the neighbour warps'
             // reads of it (their B0 k-boundary planes, one row earlier) are ordered
             // before the next write by this row's barrier.
-#if HFTW_PAIR_BAR2
-            __syncthreads();
-#endif
 #pragma unroll
             for (int kk = 0; kk < KPT; ++kk) PW1[kk] = PW2[kk];
             ibi = ibi == kPairNIB - 1 ? 0 : ibi + 1;

@@ -62,7 +62,11 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
     return v;
 }
 __device__ __forceinline__ void wait_geq(const int* p, int target) {
-    while (ld_acquire_gpu(p) < target) __nanosleep(100);
+    const unsigned long long t0 = globaltimer_ns();
+    while (ld_acquire_gpu(p) < target) {
+        __nanosleep(100);
+        spin_check(t0);
+    }
 }
 
 __device__ __forceinline__ bool wave_rows_down(const WaveArgs& a, int unit) {
@@ -156,7 +160,12 @@ __device__ __forceinline__ void wave_consumers(unsigned char* smem, const SlabGe
             const uint32_t slot = L % NS;
             mbar_wait(&full[slot], (L / NS) & 1);
         }
-        const int item = slot_item[L % NS];
+        // one reader per warp (the lane that later arrives on the slot's `empty`
+        // barrier), broadcast by shuffle: the producer's next write of this slot
+        // item is ordered after it by that arrive alone
+        int item = 0;
+        if (lane == 0) item = slot_item[L % NS];
+        item = __shfl_sync(0xffffffffu, item, 0);
         if (item < 0) break;
         const int s = item / per_step, r = item % per_step;
         const double* e = (s & 1) ? a.buf1 : a.buf0;

@@ -176,10 +176,26 @@ class SimState:
                 "energy_surf": self.energy_surf, "energy_pbl": self.energy_pbl}
 
 
-def _dptr(a: np.ndarray):
-    if a.dtype != np.float64 or not a.flags.c_contiguous:
-        raise ValueError("field buffers must be contiguous float64")
+def _dptr(a: np.ndarray, size: Optional[int] = None, writable: bool = False):
+    """ctypes pointer to a host field buffer.  The library copies whole fields
+    through it, so its type, layout and size are checked here first."""
+    if not isinstance(a, np.ndarray) or a.dtype != np.float64 or not a.flags.c_contiguous:
+        raise ValueError("field buffers must be contiguous float64 numpy arrays")
+    if size is not None and a.size != size:
+        raise ValueError(f"field buffer holds {a.size} values, the field has {size}")
+    if writable and not a.flags.writeable:
+        raise ValueError("output field buffer is read-only")
     return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _field_size(cfg: "GridConfig", name: str) -> int:
+    """Logical element count of a SimState member (weather.cpp:71, :77)."""
+    n2 = (cfg.nx + 2) * (cfg.ny + 2)
+    if name in ("energy", "energy_u"):
+        return n2 * cfg.nz
+    if name in ("energy_surf", "energy_pbl"):
+        return n2
+    raise ValueError(f"unknown field {name!r}")
 
 
 class Context:
@@ -187,13 +203,28 @@ class Context:
     reference keeps SimState on the host).  ``layout`` is "ijk" or "kij"."""
 
     def __init__(self, cfg: GridConfig, layout: str = "ijk", device: int = 0,
-                 kernel: str = "auto", px: int = 1, py: int = 1, rank: int = 0):
+                 kernel: str = "auto", px: int = 1, py: int = 1, rank: int = 0,
+                 devices: Optional[Sequence[int]] = None, _handle=None):
         """px x py > 1 creates rank `rank`'s subdomain of a decomposed run
-        (include/hftw.h, hftw_create_dist); see paper_1802_05839_b200.dist."""
+        (include/hftw.h, hftw_create_dist); see paper_1802_05839_b200.dist.
+        ``devices`` (one CUDA device per rank, repeats allowed) instead creates
+        ALL px x py ranks in this process (hftw_create_multi): the handle then
+        drives the whole decomposed grid like a single-domain context."""
         self.cfg = cfg
         self.layout = layout
         self._h = C.c_void_p()
-        if px * py == 1:
+        self._owner = _handle is None
+        if _handle is not None:  # a group's rank view (owned by the group)
+            self._h = _handle
+            return
+        if devices is not None:
+            devs = list(devices)
+            if len(devs) != px * py:
+                raise ValueError(f"{len(devs)} devices for {px} x {py} ranks")
+            arr = (C.c_int * len(devs))(*devs)
+            check(lib().hftw_create_multi(C.byref(cfg.to_c()), L.LAYOUTS[layout], px, py, arr,
+                                          C.byref(self._h)))
+        elif px * py == 1:
             check(lib().hftw_create(C.byref(cfg.to_c()), L.LAYOUTS[layout], device,
                                     C.byref(self._h)))
         else:
@@ -206,9 +237,9 @@ class Context:
         check(rc, self._h)
 
     def close(self) -> None:
-        if self._h:
+        if self._h and self._owner:
             lib().hftw_destroy(self._h)
-            self._h = C.c_void_p()
+        self._h = C.c_void_p()
 
     def __del__(self):
         try:
@@ -226,13 +257,14 @@ class Context:
         self._chk(lib().hftw_init(self._h))
 
     def upload(self, name: str, data: np.ndarray) -> None:
-        self._chk(lib().hftw_upload(self._h, L.FIELDS[name], _dptr(data)))
+        self._chk(lib().hftw_upload(self._h, L.FIELDS[name],
+                                    _dptr(data, _field_size(self.cfg, name))))
 
     def download(self, name: str, out: Optional[np.ndarray] = None) -> np.ndarray:
+        n = _field_size(self.cfg, name)
         if out is None:
-            n2 = (self.cfg.nx + 2) * (self.cfg.ny + 2)
-            out = np.empty(n2 * (self.cfg.nz if name in ("energy", "energy_u") else 1))
-        self._chk(lib().hftw_download(self._h, L.FIELDS[name], _dptr(out)))
+            out = np.empty(n)
+        self._chk(lib().hftw_download(self._h, L.FIELDS[name], _dptr(out, n, writable=True)))
         return out
 
     def upload_state(self, st: SimState) -> None:
@@ -254,17 +286,17 @@ class Context:
         """hftw_step_host: one reference_step on host arrays (logical column-major),
         with H2D, the step and D2H pipelined in row blocks.  Returns
         (energy, energy_u) after the step; energy_out may be ``energy``."""
-        n3 = (self.cfg.nx + 2) * (self.cfg.ny + 2) * self.cfg.nz
+        n3 = _field_size(self.cfg, "energy")
+        n2 = _field_size(self.cfg, "energy_surf")
         if energy_out is None:
             energy_out = np.empty(n3)
         if energy_u_out is None:
             energy_u_out = np.empty(n3)
-        for a in (energy, energy_surf, energy_pbl, energy_out, energy_u_out):
-            if a.dtype != np.float64 or not a.flags.c_contiguous:
-                raise ValueError("host arrays must be contiguous float64")
-        self._chk(lib().hftw_step_host(self._h, _dptr(energy), _dptr(energy_surf),
-                                       _dptr(energy_pbl), _dptr(energy_out),
-                                       _dptr(energy_u_out)))
+        if energy_u_out is energy or energy_u_out is energy_out:
+            raise ValueError("energy_u_out must not alias energy or energy_out")
+        self._chk(lib().hftw_step_host(self._h, _dptr(energy, n3), _dptr(energy_surf, n2),
+                                       _dptr(energy_pbl, n2), _dptr(energy_out, n3, True),
+                                       _dptr(energy_u_out, n3, True)))
         return energy_out, energy_u_out
 
     def set_timing(self, on: bool) -> None:
@@ -301,6 +333,22 @@ class Context:
 
     def set_kernel(self, name: str) -> None:
         self._chk(lib().hftw_set_kernel(self._h, L.KERNELS[name]))
+
+    def set_option(self, name: str, value: int) -> None:
+        """hftw_set_option: "multistep" (-1 never, 0 auto, 1 always) or "pair" (0/1)."""
+        self._chk(lib().hftw_set_option(self._h, L.OPTIONS[name], int(value)))
+
+    @property
+    def group_size(self) -> int:
+        """Ranks of a group context (hftw_create_multi); 1 otherwise."""
+        return lib().hftw_group_size(self._h)
+
+    def rank_context(self, r: int) -> "Context":
+        """Rank r of a group as a Context view (owned by the group: plan, timing,
+        field views).  Valid while the group is open."""
+        h = C.c_void_p()
+        self._chk(lib().hftw_group_rank(self._h, r, C.byref(h)))
+        return Context(self.cfg, layout=self.layout, _handle=h)
 
     @property
     def kernel(self) -> str:
@@ -500,13 +548,22 @@ def compare_arrays(a: ArrayObject, b: ArrayObject) -> CompareReport:
     if r.cells == 0:
         return r
     d = np.abs(a.data - b.data)
-    worst = int(np.argmax(d)) if d.size else 0
-    r.max_abs = float(d[worst])
-    if not r.max_abs > 0.0:  # the reference only moves `worst` on a strict increase
+    # `d > max_abs` (weather.cpp:196): NaN differences never win, the first of
+    # equal maxima does, and nothing below or at 0 moves `worst` off cell 0
+    dn = np.where(np.isnan(d), -np.inf, d)
+    worst = int(np.argmax(dn))
+    r.max_abs = float(dn[worst])
+    if not r.max_abs > 0.0:
         worst, r.max_abs = 0, 0.0
     diff = a.data - b.data
     sq = float(np.sum(diff * diff))
-    rng = float(a.data.max() - a.data.min())
+    # lo/hi start at a.data[0] and follow std::min/std::max, which keep their
+    # first argument when a comparison with NaN is false
+    if np.isnan(a.data[0]):
+        lo = hi = float("nan")
+    else:
+        lo, hi = float(np.nanmin(a.data)), float(np.nanmax(a.data))
+    rng = hi - lo
     if rng == 0.0:
         rng = 1.0
     r.nrmse = math.sqrt(sq / r.cells) / rng

@@ -24,19 +24,20 @@ def free_port():
     return p
 
 
-def _worker(rank, world, port, shape, grid, steps, layout, kernel, random_init, q, env=None,
+def _worker(rank, world, port, shape, grid, steps, layout, kernel, random_init, q, options=None,
             calls=None):
     import torch.distributed as dist
     from paper_1802_05839_b200.dist import DistSimulation
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    os.environ.update(env or {})
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         nx, ny, nz = shape
         cfg = W.GridConfig(nx=nx, ny=ny, nz=nz, diffusion_velocity=0.125,
                            radiation_intensity=0.37, transfer_velocity=0.013)
         sim = DistSimulation(cfg, grid[0], grid[1], layout=layout, device=0, kernel=kernel)
+        for name, value in (options or {}).items():
+            sim.ctx.set_option(name, value)
         g = O.grid_from(cfg)
         if random_init:
             rng = np.random.default_rng(7)
@@ -82,30 +83,30 @@ def test_decomposed_gpu_bitwise(shape, grid, steps, layout, kernel, random_init)
     _run_decomposed(shape, grid, steps, layout, kernel, random_init)
 
 
-@pytest.mark.parametrize("shape,grid,calls,env", [
+@pytest.mark.parametrize("shape,grid,calls,options", [
     # one launch per step for every call (what a large rank uses), mixed call lengths
-    ((131, 97, 12), (2, 2), [1, 3, 1, 2], {"HFTW_NO_WAVE": "1"}),
-    ((150, 70, 58), (1, 2), [2, 1, 4], {"HFTW_NO_WAVE": "1"}),
+    ((131, 97, 12), (2, 2), [1, 3, 1, 2], {"multistep": -1}),
+    ((150, 70, 58), (1, 2), [2, 1, 4], {"multistep": -1}),
     # odd process grids (uneven partitions, a rank between two others in both directions)
     ((97, 61, 13), (3, 1), [2, 3], {}),
     ((61, 97, 13), (1, 3), [1, 4], {}),
     ((100, 70, 9), (3, 2), [3, 2], {}),
     # single steps and multi-step launches interleaved on the same step flags
     ((131, 97, 12), (2, 2), [1, 4, 1, 3, 2], {}),
-    ((120, 90, 20), (2, 4), [3, 1, 5], {"HFTW_WAVE": "1"}),
+    ((120, 90, 20), (2, 4), [3, 1, 5], {"multistep": 1}),
 ])
-def test_decomposed_call_mix_bitwise(shape, grid, calls, env):
-    _run_decomposed(shape, grid, sum(calls), "ijk", "fused_tma", True, env, calls)
+def test_decomposed_call_mix_bitwise(shape, grid, calls, options):
+    _run_decomposed(shape, grid, sum(calls), "ijk", "fused_tma", True, options, calls)
 
 
-def _run_decomposed(shape, grid, steps, layout, kernel, random_init, env=None, calls=None):
+def _run_decomposed(shape, grid, steps, layout, kernel, random_init, options=None, calls=None):
     import torch.multiprocessing as mp
     world = grid[0] * grid[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
     procs = [ctx.Process(target=_worker, args=(r, world, port, shape, grid, steps, layout, kernel,
-                                               random_init, q, env, calls))
+                                               random_init, q, options, calls))
              for r in range(world)]
     for p in procs:
         p.start()

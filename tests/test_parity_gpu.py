@@ -25,8 +25,10 @@ def cfg_of(d):
     return W.GridConfig(**d)
 
 
-def run_device(cfg, steps, layout="ijk", kernel="auto", init_state=None):
+def run_device(cfg, steps, layout="ijk", kernel="auto", init_state=None, options=None):
     with W.Context(cfg, layout=layout, kernel=kernel) as ctx:
+        for name, value in (options or {}).items():
+            ctx.set_option(name, value)
         if init_state is None:
             ctx.init()
         else:
@@ -371,6 +373,7 @@ def test_multi_step_launch_vs_oracle(coracle, shape, steps):
                  rng.uniform(150, 350, n2), rng.uniform(150, 350, n2))
     want = coracle.steps(g, s0, 2 * steps).fields()
     with W.Context(cfg, kernel="fused_tma") as ctx:
+        ctx.set_option("multistep", 1)
         for name, arr in s0.fields().items():
             ctx.upload(name, np.ascontiguousarray(arr))
         ctx.set_timing(True)
@@ -382,13 +385,12 @@ def test_multi_step_launch_vs_oracle(coracle, shape, steps):
     assert_same(got, want, f"{shape}/wave/{steps}")
 
 
-@pytest.mark.parametrize("kernel,steps,wave", [("auto", 7, "0"), ("fused_tma", 6, "0"),
-                                               ("fused_tma", 6, "1")])
-def test_asuca_random_state_non_default_constants(coracle, kernel, steps, wave, monkeypatch):
+@pytest.mark.parametrize("kernel,steps,wave", [("auto", 7, 0), ("fused_tma", 6, 0),
+                                               ("fused_tma", 6, 1)])
+def test_asuca_random_state_non_default_constants(coracle, kernel, steps, wave):
     """BASELINE's full size from a random state with non-default constants: the
     pair passes (auto), one launch per step (fused_tma) and the multi-step launch
-    (fused_tma, HFTW_WAVE=1: at this size AUTO prefers one launch per step), bitwise."""
-    monkeypatch.setenv("HFTW_WAVE", wave)
+    (fused_tma, multistep=1: at this size AUTO prefers one launch per step), bitwise."""
     rng = np.random.default_rng(1802)
     cfg = W.GridConfig(nx=1581, ny=1301, nz=58, diffusion_velocity=0.1375,
                        radiation_intensity=-0.21, transfer_velocity=0.047,
@@ -398,7 +400,7 @@ def test_asuca_random_state_non_default_constants(coracle, kernel, steps, wave, 
     s0 = O.State(rng.uniform(150, 350, n3), rng.uniform(150, 350, n3),
                  rng.uniform(150, 350, n2), rng.uniform(150, 350, n2))
     want = coracle.steps(g, s0, steps).fields()
-    got = run_device(cfg, steps, "ijk", kernel, s0.fields())
+    got = run_device(cfg, steps, "ijk", kernel, s0.fields(), {"multistep": wave})
     assert_same(got, want, f"asuca/{kernel}/{steps}")
 
 
