@@ -234,6 +234,7 @@ int hftw_simulate(hftw_ctx* ctx, double start_time, double end_time, double time
  * static sf/pb halos), and a per-direction step flag orders the pushes.  The
  * result is bitwise identical to the single-domain run. */
 enum hftw_dir { HFTW_W = 0, HFTW_E = 1, HFTW_S = 2, HFTW_N = 3 };
+enum hftw_diag { HFTW_SW = 0, HFTW_SE = 1, HFTW_NW = 2, HFTW_NE = 3 };
 
 typedef struct hftw_plan {
     int32_t px, py, rx, ry, rank;
@@ -244,6 +245,12 @@ typedef struct hftw_plan {
     int32_t nbr[4];              /* neighbour rank per hftw_dir, -1 = cyclic partner is local */
     int32_t send_slot[4];        /* my face lands in the neighbour at this local column (W/E) or row (S/N) */
     int64_t face_lo[4], face_hi[4]; /* local range along each face (j for W/E, i for S/N) */
+    /* two-step (pair) passes read 2-deep halos: */
+    int32_t depth[4];            /* layers my face sends (and receives): 2 to an interior
+                                    neighbour, 1 to a wrap partner (its far slot), 0 none */
+    int32_t diag[4];             /* diagonal neighbour SW, SE, NW, NE (-1: none); it gets my
+                                    corner cell (1,1) / (nx,1) / (1,ny) / (nx,ny) column */
+    int32_t diag_slot[4][2];     /* (i, j) where that corner column lands in it */
 } hftw_plan;
 
 /* Host-only (no GPU needed): the plan of `rank` in a px x py decomposition. */

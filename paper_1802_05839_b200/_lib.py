@@ -42,13 +42,16 @@ class hftw_plan(C.Structure):
                 ("own_n", C.c_int32), ("wfar", C.c_int32), ("efar", C.c_int32),
                 ("sfar", C.c_int32), ("nfar", C.c_int32), ("nbr", C.c_int32 * 4),
                 ("send_slot", C.c_int32 * 4), ("face_lo", C.c_int64 * 4),
-                ("face_hi", C.c_int64 * 4)]
+                ("face_hi", C.c_int64 * 4), ("depth", C.c_int32 * 4), ("diag", C.c_int32 * 4),
+                ("diag_slot", (C.c_int32 * 2) * 4)]
 
     def to_dict(self):
         d = {}
         for f, _ in self._fields_:
             v = getattr(self, f)
-            d[f] = list(v) if isinstance(v, C.Array) else v
+            if isinstance(v, C.Array):
+                v = [list(x) if isinstance(x, C.Array) else x for x in v]
+            d[f] = v
         return d
 
 

@@ -67,6 +67,9 @@ constexpr int kPairKPT = HFTW_PAIR_KPT; // planes per thread of the pair kernel 
 // plus the geometry needed to address their halo slots.
 struct PeerDesc {
     cudaIpcMemHandle_t buf[2], sf, flags; // sf's allocation also holds pb (n2 further)
+    cudaIpcMemHandle_t gpub;              // published P' of the pair passes (if any)
+    int has_gpub;
+    long long gpub_n, gcol_n;             // its doubles per parity / of the gcol part
     long long off3, off2, si, sj, sk, s2j, n2;
     hftw_plan plan;
     int magic;
@@ -79,6 +82,8 @@ struct PeerMap {
     double* sf = nullptr;                // at its logical (0,0)
     double* pb = nullptr;
     unsigned long long* flags = nullptr;
+    double* gpub = nullptr;              // its published P' (two pass parities)
+    long long gpub_n = 0, gcol_n = 0;    // its sizes (its subdomain may be a row / column longer)
     long long si = 0, sj = 0, sk = 0, s2j = 0;
 };
 
@@ -135,8 +140,12 @@ struct hftw_ctx {
     int pair_nstrips = 0;
     CUtensorMap tm_sfpb{}, tm_sfpbf{};  // [sf; pb]: slab rows / far pair
     int* d_pair = nullptr;      // sched[2] + cnt_col[nchunks] + cnt_row[nstrips]
-    double* gcol = nullptr;     // [4][ny+2][nz]
-    double* grow = nullptr;     // [4][nz][nx+2]
+    // published ghost-adjacent P' of a pass, two parities (decomposed passes
+    // alternate so that a wrap partner may still read the previous one):
+    // [parity][gcol [4][ny+2][nz] | grow [4][nz][nx+2]]
+    double* gpub = nullptr;
+    size_t gpub_n = 0;          // doubles per parity
+    long long pass_count = 0;   // pair passes since the last exchange (parity)
 
     // multi-step wavefront launch (weather_wave.cuh): single-domain IJK
     bool wave_ok = false;
@@ -155,9 +164,9 @@ struct hftw_ctx {
     std::vector<TimedLaunch> tev;
 
     // decomposed run
-    unsigned long long* flags = nullptr; // [4] step flags written by the neighbours
+    unsigned long long* flags = nullptr; // [kFlags] step flags written by the neighbours
     int* done = nullptr;                 // CTAs finished in the current launch
-    PeerMap peer[4];
+    PeerMap peer[hftw::kNbrs];          // faces W E S N, then corners SW SE NW NE
     std::vector<void*> ipc_opened;
     bool connected = false;
     bool halo_dirty = false;             // fields changed since the last exchange
@@ -250,15 +259,20 @@ Halo make_halo(const hftw_ctx* c, int dst) {
     Halo h{};
     h.active = c->dist ? 1 : 0;
     if (!c->dist) return h;
-    for (int d = 0; d < 4; ++d) {
-        const PeerMap& m = c->peer[d];
+    for (int q = 0; q < hftw::kNbrs; ++q) {
+        const PeerMap& m = c->peer[q];
         if (m.rank < 0) continue;
-        h.nb[d] = m.buf[dst];
-        h.nsi[d] = m.si;
-        h.nsj[d] = m.sj;
-        h.nsk[d] = m.sk;
+        h.nb[q] = m.buf[dst];
+        h.nsi[q] = m.si;
+        h.nsj[q] = m.sj;
+        h.nsk[q] = m.sk;
+        h.nb_flags[q] = m.flags;
+    }
+    for (int d = 0; d < 4; ++d) {
         h.slot[d] = c->plan.send_slot[d];
-        h.nb_flags[d] = m.flags;
+        h.depth[d] = c->plan.depth[d];
+        h.cslot[d][0] = c->plan.diag_slot[d][0];
+        h.cslot[d][1] = c->plan.diag_slot[d][1];
     }
     h.my_flags = c->flags;
     h.done = c->done;
@@ -459,13 +473,20 @@ int setup_tma(hftw_ctx* c) {
 // intermediate row buffers.  Leaves pair_ok = false otherwise.
 int setup_pair(hftw_ctx* c) {
     c->pair_ok = false;
-    if (!c->tma_ok || c->layout != HFTW_IJK || c->dist || c->nz > hftw::kPairKG * kPairKPT)
-        return HFTW_OK;
+    if (!c->tma_ok || c->layout != HFTW_IJK || c->nz > hftw::kPairKG * kPairKPT) return HFTW_OK;
+    if (c->dist) {
+        // every rank of the decomposition must take the same decision: two-step
+        // passes need 2 owned cells next to every interior face of every rank
+        // (the smallest balanced part is floor(n / p))
+        const hftw_plan& p = c->plan;
+        if ((p.px > 1 && c->g.nx / p.px < 2) || (p.py > 1 && c->g.ny / p.py < 2)) return HFTW_OK;
+    }
     auto enc = encode_fn();
     int smem_optin = 0;
     CUDA_TRY(c, cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin,
                                        c->device));
-    auto kern = hftw::step_pair_kernel<kPairKPT>;
+    auto kern = c->dist ? hftw::step_pair_kernel<kPairKPT, true>
+                        : hftw::step_pair_kernel<kPairKPT, false>;
     cudaFuncAttributes fa{};
     CUDA_TRY(c, cudaFuncGetAttributes(&fa, kern));
     const int nz = (int)c->nz;
@@ -552,8 +573,8 @@ int setup_pair(hftw_ctx* c) {
     const size_t ints = 2 + (size_t)c->pair_nchunks + (size_t)c->pair_nstrips;
     CUDA_TRY(c, cudaMalloc(&c->d_pair, ints * sizeof(int)));
     CUDA_TRY(c, cudaMemset(c->d_pair, 0, ints * sizeof(int)));
-    CUDA_TRY(c, cudaMalloc(&c->gcol, (size_t)(4 * (ny + 2) * c->nz) * sizeof(double)));
-    CUDA_TRY(c, cudaMalloc(&c->grow, (size_t)(4 * c->nz * (c->lnx + 2)) * sizeof(double)));
+    c->gpub_n = (size_t)(4 * (ny + 2) * c->nz) + (size_t)(4 * c->nz * (c->lnx + 2));
+    CUDA_TRY(c, cudaMalloc(&c->gpub, 2 * c->gpub_n * sizeof(double)));
     // the compile-time row shapes cover groups of KPT-1 .. KPT planes; other nz run
     // the generic (runtime plane checks) path, which AUTO leaves to the TMA kernel
     c->pair_fast = c->nz >= (long long)hftw::kPairKG * (kPairKPT - 1);
@@ -585,6 +606,11 @@ int timing_mark(hftw_ctx* c, int kind, bool begin, int64_t steps = 1) {
     return HFTW_OK;
 }
 
+// The published-P' buffer of a pass (two parities of `per` doubles; see hftw_ctx::gpub).
+double* gpub_of(double* base, size_t per, long long pass) {
+    return base + (size_t)(pass & 1) * per;
+}
+
 // Two fused steps in one launch: buf[src] -> buf[src ^ 1] = step(step(buf[src])).
 int launch_pair(hftw_ctx* c, int src) {
     Dom d = make_dom(c);
@@ -600,16 +626,79 @@ int launch_pair(hftw_ctx* c, int src) {
     a.sched = c->d_pair;
     a.cnt_col = c->d_pair + 2;
     a.cnt_row = c->d_pair + 2 + c->pair_nchunks;
-    a.gcol = c->gcol;
-    a.grow = c->grow;
+    double* pub = gpub_of(c->gpub, c->gpub_n, c->pass_count);
+    a.gcol = pub;
+    a.grow = pub + 4 * (c->lny + 2) * c->nz;
+    const Halo h = make_halo(c, src ^ 1); // pushes into the neighbours' e_{s+2}, waits >= s
     int rc = timing_mark(c, 1, true);
     if (rc) return rc;
-    auto kern = hftw::step_pair_kernel<kPairKPT>;
+    auto kern = c->dist ? hftw::step_pair_kernel<kPairKPT, true>
+                        : hftw::step_pair_kernel<kPairKPT, false>;
     kern<<<c->pair_ctas, hftw::kPairThreads, c->pair_smem, c->stream>>>(
         c->tm_e2[src], c->tm_sfpb, c->tm_ef[src], c->tm_sfpbf, e3(c, src), e3(c, src ^ 1), sf2(c),
-        pb2(c), d, a);
+        pb2(c), d, a, h);
     CUDA_TRY(c, cudaGetLastError());
     return timing_mark(c, 1, false, 2);
+}
+
+// Decomposed pair pass, second launch: the ghost cells of e_{s+2} from this
+// rank's and the wrap partners' published P', their pushes, and the release
+// of the pass to every neighbour (weather_pair.cuh, pair_ghost_kernel).
+int launch_pair_ghost(hftw_ctx* c, int dst) {
+    const Dom d = make_dom(c);
+    Halo h = make_halo(c, dst);
+    h.step = c->step_count + 1; // releases s + 2
+    hftw::PairGhostArgs g{};
+    const long long ncol = 4 * (c->lny + 2) * c->nz;
+    double* mine = gpub_of(c->gpub, c->gpub_n, c->pass_count);
+    g.gcol = mine;
+    g.grow = mine + ncol;
+    // the wrap partner of each owned edge: a remote rank (its published P' over
+    // NVLink, after its "published" flag), or this rank along an undivided axis.
+    // The partner along i has this rank's rows, the one along j its columns.
+    const hftw_plan& p = c->plan;
+    const int dirs[4] = {HFTW_W, HFTW_E, HFTW_S, HFTW_N};
+    const double* part[4];
+    for (int q : dirs) {
+        const PeerMap& m = c->peer[q];
+        const bool remote = m.rank >= 0 && p.depth[q] == 1;
+        if (remote && !m.gpub)
+            return fail(c, HFTW_ESTATE, "rank %d has no published-P' buffer", m.rank);
+        const double* base = remote ? gpub_of(m.gpub, (size_t)m.gpub_n, c->pass_count) : mine;
+        part[q] = q < 2 ? base : base + (remote ? m.gcol_n : ncol);
+        g.wait[q] = remote ? 1 : 0;
+    }
+    g.gcol_w = part[HFTW_W];
+    g.gcol_e = part[HFTW_E];
+    g.grow_s = part[HFTW_S];
+    g.grow_n = part[HFTW_N];
+    g.pub = c->step_count + 2;
+    const long long cells = 2 * (c->lny + 2 + c->lnx) * c->nz;
+    const int blocks = (int)std::max<long long>(
+        1, std::min<long long>((cells + 255) / 256, (long long)c->num_sms * 2));
+    hftw::pair_ghost_kernel<<<blocks, 256, 0, c->stream>>>(e3(c, dst), d, h, g);
+    CUDA_TRY(c, cudaGetLastError());
+    return HFTW_OK;
+}
+
+// Two-step passes of an n-step call: pairs, then one or two single steps (the
+// last step is a single-step launch so that energy_u, the physics of the field
+// before it, stays derivable from the ping-pong partner).
+int64_t pair_passes(int64_t nsteps) { return nsteps >= 3 ? (nsteps - 1) / 2 : 0; }
+
+// One pass: phase bit 0 launches the pair kernel, bit 1 (decomposed) the ghost
+// kernel, and then the bookkeeping.  A group on one device runs bit 0 for every
+// rank before bit 1 for any (the ghost kernels wait for the wrap partners').
+int pair_pass(hftw_ctx* c, int phase) {
+    int rc;
+    if ((phase & 1) && (rc = launch_pair(c, c->cur))) return rc;
+    if (phase & 2) {
+        if (c->dist && (rc = launch_pair_ghost(c, c->cur ^ 1))) return rc;
+        c->cur ^= 1;
+        c->step_count += 2;
+        ++c->pass_count;
+    }
+    return HFTW_OK;
 }
 
 // K steps per launch with the TMA kernel's tiling (weather_wave.cuh): single
@@ -880,10 +969,36 @@ int make_plan(const hftw_grid* g, int px, int py, int rank, hftw_plan* o) {
     p.send_slot[HFTW_E] = rxe == 0 ? -1 : 0;                               // its W-far / W slot
     p.send_slot[HFTW_S] = rys == py - 1 ? (int)lny_s + 2 : (int)lny_s + 1;
     p.send_slot[HFTW_N] = ryn == 0 ? -1 : 0;
+    // faces span the owned cells along them, the owned global ghost row /
+    // column included: a two-step pass's halo intermediates read them
     p.face_lo[HFTW_W] = p.face_lo[HFTW_E] = p.own_s ? 0 : 1;
     p.face_hi[HFTW_W] = p.face_hi[HFTW_E] = p.own_n ? p.lny + 1 : p.lny;
-    p.face_lo[HFTW_S] = p.face_lo[HFTW_N] = 1;
-    p.face_hi[HFTW_S] = p.face_hi[HFTW_N] = p.lnx;
+    p.face_lo[HFTW_S] = p.face_lo[HFTW_N] = p.own_w ? 0 : 1;
+    p.face_hi[HFTW_S] = p.face_hi[HFTW_N] = p.own_e ? p.lnx + 1 : p.lnx;
+    // layers per face: a wrap partner needs only its far slot (1); an interior
+    // neighbour reads 2 layers in a two-step pass (1 where this rank is 1 wide)
+    const auto layers = [](int np, bool own, long long ext) {
+        return np == 1 ? 0 : own ? 1 : (int)std::min<long long>(2, ext);
+    };
+    p.depth[HFTW_W] = layers(px, p.own_w, p.lnx);
+    p.depth[HFTW_E] = layers(px, p.own_e, p.lnx);
+    p.depth[HFTW_S] = layers(py, p.own_s, p.lny);
+    p.depth[HFTW_N] = layers(py, p.own_n, p.lny);
+    // diagonal neighbours across two interior faces get one corner column
+    const bool iw = px > 1 && !p.own_w, ie = px > 1 && !p.own_e;
+    const bool is = py > 1 && !p.own_s, in = py > 1 && !p.own_n;
+    p.diag[HFTW_SW] = iw && is ? rys * px + rxw : -1;
+    p.diag[HFTW_SE] = ie && is ? rys * px + rxe : -1;
+    p.diag[HFTW_NW] = iw && in ? ryn * px + rxw : -1;
+    p.diag[HFTW_NE] = ie && in ? ryn * px + rxe : -1;
+    p.diag_slot[HFTW_SW][0] = (int)lnx_w + 1;
+    p.diag_slot[HFTW_SW][1] = (int)lny_s + 1;
+    p.diag_slot[HFTW_SE][0] = 0;
+    p.diag_slot[HFTW_SE][1] = (int)lny_s + 1;
+    p.diag_slot[HFTW_NW][0] = (int)lnx_w + 1;
+    p.diag_slot[HFTW_NW][1] = 0;
+    p.diag_slot[HFTW_NE][0] = 0;
+    p.diag_slot[HFTW_NE][1] = 0;
     *o = p;
     return HFTW_OK;
 }
@@ -961,13 +1076,13 @@ int create_common(const hftw_grid* g, int layout, int device, const hftw_plan& p
     if (cudaMalloc(&c->sf, 2 * c->n2 * sizeof(double)) != cudaSuccess)
         return bail(fail(c, HFTW_ENOMEM, "cudaMalloc of 2D fields failed"));
     c->pb = c->sf + c->n2;
-    if (cudaMalloc(&c->flags, 4 * sizeof(unsigned long long)) != cudaSuccess ||
+    if (cudaMalloc(&c->flags, hftw::kFlags * sizeof(unsigned long long)) != cudaSuccess ||
         cudaMalloc(&c->done, sizeof(int)) != cudaSuccess)
         return bail(fail(c, HFTW_ENOMEM, "cudaMalloc of halo flags failed"));
     for (int b = 0; b < 2; ++b) cudaMemsetAsync(c->buf[b], 0, c->n3 * sizeof(double), c->stream);
     cudaMemsetAsync(c->sf, 0, c->n2 * sizeof(double), c->stream);
     cudaMemsetAsync(c->pb, 0, c->n2 * sizeof(double), c->stream);
-    cudaMemsetAsync(c->flags, 0, 4 * sizeof(unsigned long long), c->stream);
+    cudaMemsetAsync(c->flags, 0, hftw::kFlags * sizeof(unsigned long long), c->stream);
     cudaMemsetAsync(c->done, 0, sizeof(int), c->stream);
     if (cudaStreamSynchronize(c->stream) != cudaSuccess)
         return bail(fail(c, HFTW_ECUDA, "initial memset failed"));
@@ -981,11 +1096,14 @@ int create_common(const hftw_grid* g, int layout, int device, const hftw_plan& p
 
 // ---- group contexts (hftw_create_multi): every rank in this process -------
 
+// Rank of the neighbour in direction q (faces W E S N, then corners SW SE NW NE).
+int nbr_rank(const hftw_plan& p, int q) { return q < 4 ? p.nbr[q] : p.diag[q - 4]; }
+
 // Map the neighbours of rank c from the other ranks' device pointers (the
 // in-process counterpart of hftw_peer_connect's IPC mappings).
 void connect_local(hftw_ctx* c, const std::vector<hftw_ctx*>& ranks) {
-    for (int d = 0; d < 4; ++d) {
-        const int r = c->plan.nbr[d];
+    for (int d = 0; d < hftw::kNbrs; ++d) {
+        const int r = nbr_rank(c->plan, d);
         if (r < 0) {
             c->peer[d] = PeerMap{};
             continue;
@@ -997,6 +1115,9 @@ void connect_local(hftw_ctx* c, const std::vector<hftw_ctx*>& ranks) {
         m.sf = n->sf + n->off2;
         m.pb = n->pb + n->off2;
         m.flags = n->flags;
+        m.gpub = n->gpub;
+        m.gpub_n = (long long)n->gpub_n;
+        m.gcol_n = 4 * (n->lny + 2) * n->nz;
         m.si = n->si;
         m.sj = n->sj;
         m.sk = n->sk;
@@ -1070,8 +1191,8 @@ int create_group(const hftw_grid* g, int layout, int px, int py, const int* devi
             }
     // peer access between neighbouring ranks on distinct devices (NVLink)
     for (int r = 0; r < n; ++r)
-        for (int d = 0; d < 4; ++d) {
-            const int q = c->ranks[(size_t)r]->plan.nbr[d];
+        for (int d = 0; d < hftw::kNbrs; ++d) {
+            const int q = nbr_rank(c->ranks[(size_t)r]->plan, d);
             if (q < 0 || dev[(size_t)q] == dev[(size_t)r]) continue;
             int can = 0;
             cudaDeviceCanAccessPeer(&can, dev[(size_t)r], dev[(size_t)q]);
@@ -1127,6 +1248,19 @@ int group_step(hftw_ctx* c, int64_t nsteps) {
             break;
         }
     if (c->interleave) {
+        // ranks sharing a device: every launch of a pass for all ranks, in rank
+        // order, before any launch that waits for it
+        hftw_ctx* r0 = c->ranks[0];
+        if (resolved_kernel(r0) == HFTW_KERNEL_FUSED_PAIR && r0->pair_ok) {
+            const int64_t pairs = pair_passes(nsteps);
+            for (int64_t p = 0; p < pairs; ++p)
+                for (int phase : {1, 2})
+                    for (hftw_ctx* r : c->ranks) {
+                        RANK_TRY(c, r, check_ctx(r));
+                        RANK_TRY(c, r, pair_pass(r, phase));
+                    }
+            nsteps -= 2 * pairs;
+        }
         for (int64_t s = 0; s < nsteps; ++s)
             for (hftw_ctx* r : c->ranks) RANK_TRY(c, r, hftw_step(r, 1));
     } else {
@@ -1335,8 +1469,7 @@ void hftw_destroy(hftw_ctx* c) {
     if (c->d_sched) cudaFree(c->d_sched);
     if (c->d_pair) cudaFree(c->d_pair);
     if (c->d_wave) cudaFree(c->d_wave);
-    if (c->gcol) cudaFree(c->gcol);
-    if (c->grow) cudaFree(c->grow);
+    if (c->gpub) cudaFree(c->gpub);
     for (auto& t : c->tev) {
         cudaEventDestroy(t.a);
         cudaEventDestroy(t.b);
@@ -1472,12 +1605,9 @@ int hftw_step(hftw_ctx* c, int64_t nsteps) {
         // pairs, then one or two single steps: the last step is a single-step
         // launch so that energy_u (physics of the field before it) stays
         // derivable from the ping-pong partner
-        const int64_t pairs = nsteps >= 3 ? (nsteps - 1) / 2 : 0;
-        for (int64_t p = 0; p < pairs; ++p) {
-            if ((rc = launch_pair(c, c->cur))) return rc;
-            c->cur ^= 1;
-            c->step_count += 2;
-        }
+        const int64_t pairs = pair_passes(nsteps);
+        for (int64_t p = 0; p < pairs; ++p)
+            if ((rc = pair_pass(c, 3))) return rc;
         nsteps -= 2 * pairs;
     }
     const bool multistep = c->opt_multistep > 0 || (c->opt_multistep == 0 && c->wave_pref);
@@ -1770,6 +1900,10 @@ int hftw_peer_export(hftw_ctx* c, void* out) {
     CUDA_TRY(c, cudaIpcGetMemHandle(&pd.sf, c->sf));
     pd.n2 = (long long)c->n2;
     CUDA_TRY(c, cudaIpcGetMemHandle(&pd.flags, c->flags));
+    pd.has_gpub = c->gpub ? 1 : 0;
+    pd.gpub_n = (long long)c->gpub_n;
+    pd.gcol_n = 4 * (c->lny + 2) * c->nz;
+    if (c->gpub) CUDA_TRY(c, cudaIpcGetMemHandle(&pd.gpub, c->gpub));
     pd.off3 = c->off3;
     pd.off2 = c->off2;
     pd.si = c->si;
@@ -1789,9 +1923,9 @@ int hftw_peer_connect(hftw_ctx* c, const void* all, int world) {
     if (!all || world != c->plan.px * c->plan.py)
         return fail(c, HFTW_EINVAL, "need %d descriptors, got %d", c->plan.px * c->plan.py, world);
     const PeerDesc* pds = static_cast<const PeerDesc*>(all);
-    std::map<int, PeerMap> opened; // a rank can be the neighbour in two directions
-    for (int d = 0; d < 4; ++d) {
-        const int r = c->plan.nbr[d];
+    std::map<int, PeerMap> opened; // a rank can be the neighbour in several directions
+    for (int d = 0; d < hftw::kNbrs; ++d) {
+        const int r = nbr_rank(c->plan, d);
         if (r < 0) {
             c->peer[d] = PeerMap{};
             continue;
@@ -1816,6 +1950,13 @@ int hftw_peer_connect(hftw_ctx* c, const void* all, int world) {
             CUDA_TRY(c, cudaIpcOpenMemHandle(&p, pd.flags, cudaIpcMemLazyEnablePeerAccess));
             c->ipc_opened.push_back(p);
             m.flags = static_cast<unsigned long long*>(p);
+            if (pd.has_gpub) {
+                CUDA_TRY(c, cudaIpcOpenMemHandle(&p, pd.gpub, cudaIpcMemLazyEnablePeerAccess));
+                c->ipc_opened.push_back(p);
+                m.gpub = static_cast<double*>(p);
+                m.gpub_n = pd.gpub_n;
+                m.gcol_n = pd.gcol_n;
+            }
             m.si = pd.si;
             m.sj = pd.sj;
             m.sk = pd.sk;
@@ -1840,26 +1981,24 @@ int hftw_exchange(hftw_ctx* c) {
     if (!c->connected) return fail(c, HFTW_ESTATE, "peers not connected (hftw_peer_connect)");
     Dom d = make_dom(c);
     Halo h = make_halo(c, c->cur); // faces of the CURRENT field into the neighbours' current buffer
-    double* nsf[4] = {nullptr, nullptr, nullptr, nullptr};
-    double* npb[4] = {nullptr, nullptr, nullptr, nullptr};
-    long long n2j[4] = {0, 0, 0, 0};
-    for (int k = 0; k < 4; ++k)
-        if (c->peer[k].rank >= 0) {
-            nsf[k] = c->peer[k].sf;
-            npb[k] = c->peer[k].pb;
-            n2j[k] = c->peer[k].s2j;
+    hftw::Halo2D h2{};
+    for (int q = 0; q < hftw::kNbrs; ++q)
+        if (c->peer[q].rank >= 0) {
+            h2.sf[q] = c->peer[q].sf;
+            h2.pb[q] = c->peer[q].pb;
+            h2.s2j[q] = c->peer[q].s2j;
         }
     const Box o = owned_box(c);
-    const long long n = (2 * (o.j1 - o.j0 + 1) + 2 * c->lnx) * c->nz;
-    hftw::exchange_kernel<<<grid_for(c, n), 256, 0, c->stream>>>(
-        e3(c, c->cur), sf2(c), pb2(c), d, h, nsf[0], nsf[1], nsf[2], nsf[3], npb[0], npb[1],
-        npb[2], npb[3], n2j[0], n2j[1], n2j[2], n2j[3], (int)o.j0, (int)o.j1);
+    const long long n = (o.i1 - o.i0 + 1) * (o.j1 - o.j0 + 1) * c->nz;
+    hftw::exchange_kernel<<<grid_for(c, n), 256, 0, c->stream>>>(e3(c, c->cur), sf2(c), pb2(c), d,
+                                                                  h, h2);
     CUDA_TRY(c, cudaGetLastError());
     // a fresh epoch: step flags restart from zero on every rank
-    CUDA_TRY(c, cudaMemsetAsync(c->flags, 0, 4 * sizeof(unsigned long long), c->stream));
+    CUDA_TRY(c, cudaMemsetAsync(c->flags, 0, hftw::kFlags * sizeof(unsigned long long), c->stream));
     CUDA_TRY(c, cudaMemsetAsync(c->done, 0, sizeof(int), c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     c->step_count = 0;
+    c->pass_count = 0;
     c->halo_dirty = false;
     return HFTW_OK;
 }

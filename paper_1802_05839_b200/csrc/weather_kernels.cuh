@@ -119,25 +119,36 @@ __device__ __forceinline__ Owned owned(const Dom& d) {
 }
 
 //------------------------------------------------------------------------------
-// Multi-GPU halo protocol (2D I x J decomposition, one process per GPU).
+// Multi-GPU halo protocol (2D I x J decomposition, one rank per GPU).
 //
 // Every launch computes step `step` (0-based) from buffer A into buffer B.
-// A rank's first/last inner column and row of B are stored straight into the
-// neighbours' copy of B (their halo slots, mapped over NVLink with CUDA IPC)
-// as they are computed.  When all CTAs of the launch are done, the last one
-// releases flag[opp(d)] = step + 1 in each neighbour d.  Work that reads a
-// halo slot of A, or pushes into a neighbour, first acquires flag[d] >= step:
-// the neighbour has finished step-1, so its pushes into A are complete and it
-// no longer reads the B slots we are about to overwrite (WAR safety with two
-// buffers).  Interior work never waits, so the exchange overlaps it.
+// Owned cells of B near a face are stored straight into the neighbours' copy
+// of B (their halo slots, mapped over NVLink: CUDA IPC across processes, plain
+// peer pointers within one) as they are computed: `depth` layers per face (2
+// to an interior neighbour, so that a two-step pass finds a 2-deep halo; 1 to
+// a wrap partner, whose far slot needs only the first inner column / row),
+// and the corner cell column to a diagonal neighbour across two interior
+// faces.  When all CTAs of the launch are done, the last one releases
+// flag[opp(d)] = step + 1 in each neighbour d.  Work that reads a halo slot of
+// A, or pushes into a neighbour, first acquires flag[d] >= step from every
+// neighbour: they have finished step-1, so their pushes into A are complete
+// and they no longer read the B slots we are about to overwrite (WAR safety
+// with two buffers).  Interior work never waits, so the exchange overlaps it.
 //------------------------------------------------------------------------------
+constexpr int kNbrs = 8;      // W E S N faces, then SW SE NW NE corners
+constexpr int kPubFlag = 8;   // my_flags[kPubFlag + d]: pass published by the wrap partner d
+constexpr int kFlags = 12;
+__host__ __device__ inline int opp_dir(int q) { return q < 4 ? q ^ 1 : q ^ 3; }
+
 struct Halo {
     int active;                      // decomposed run
-    double* nb[4];                   // neighbour's destination buffer at its logical (0,0,1)
-    long long nsi[4], nsj[4], nsk[4];
-    int slot[4];                     // column (W/E) or row (S/N) my face lands in
-    unsigned long long* my_flags;    // [4], written by the neighbours
-    unsigned long long* nb_flags[4]; // neighbour's flag array
+    double* nb[kNbrs];               // neighbour's destination buffer at its logical (0,0,1)
+    long long nsi[kNbrs], nsj[kNbrs], nsk[kNbrs];
+    int slot[4];                     // layer-1 column (W/E) or row (S/N) of my face in it
+    int depth[4];                    // layers per face
+    int cslot[4][2];                 // (i, j) of my corner column in the diagonal neighbour
+    unsigned long long* my_flags;    // [kFlags], written by the neighbours
+    unsigned long long* nb_flags[kNbrs]; // neighbour's flag array
     int* done;                       // CTAs of this launch that finished
     long long step;
 };
@@ -163,31 +174,45 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 __device__ __forceinline__ void spin_check(unsigned long long t0) {
     if (globaltimer_ns() - t0 > kSpinLimitNs) __trap();
 }
-
-// Wait until every neighbour in `mask` (bit d = hftw_dir d) finished step-1.
-__device__ __forceinline__ void halo_wait(const Halo& h, int mask) {
-    if (!h.active) return;
-    for (int d = 0; d < 4; ++d) {
-        if (!((mask >> d) & 1) || !h.nb[d]) continue;
-        const unsigned long long t0 = globaltimer_ns();
-        while ((long long)ld_acquire_sys(&h.my_flags[d]) < h.step) {
-            __nanosleep(64);
-            spin_check(t0);
-        }
+__device__ __forceinline__ void wait_flag(const unsigned long long* f, long long target) {
+    const unsigned long long t0 = globaltimer_ns();
+    while ((long long)ld_acquire_sys(f) < target) {
+        __nanosleep(64);
+        spin_check(t0);
     }
 }
 
-// Store a freshly computed owned cell into the neighbours that need it.
+// Wait until every neighbour finished step-1 (mask != 0: a unit on the rim).
+__device__ __forceinline__ void halo_wait(const Halo& h, int mask) {
+    if (!h.active || !mask) return;
+    for (int q = 0; q < kNbrs; ++q)
+        if (h.nb[q]) wait_flag(&h.my_flags[q], h.step);
+}
+
+// Store a freshly computed OWNED cell into the neighbours that need it.
 __device__ __forceinline__ void halo_push(const Halo& h, const Dom& d, int i, int j, int k,
                                           double v) {
     if (!h.active) return;
     const long long kk = (long long)(k - 1);
-    if (h.nb[0] && i == 1) h.nb[0][h.slot[0] * h.nsi[0] + j * h.nsj[0] + kk * h.nsk[0]] = v;
-    if (h.nb[1] && i == d.nx) h.nb[1][h.slot[1] * h.nsi[1] + j * h.nsj[1] + kk * h.nsk[1]] = v;
-    if (i >= 1 && i <= d.nx) {
-        if (h.nb[2] && j == 1) h.nb[2][i * h.nsi[2] + h.slot[2] * h.nsj[2] + kk * h.nsk[2]] = v;
-        if (h.nb[3] && j == d.ny) h.nb[3][i * h.nsi[3] + h.slot[3] * h.nsj[3] + kk * h.nsk[3]] = v;
+    auto put = [&](int q, long long ti, long long tj) {
+        h.nb[q][ti * h.nsi[q] + tj * h.nsj[q] + kk * h.nsk[q]] = v;
+    };
+    if (h.nb[0] && i >= 1 && i <= h.depth[0]) put(0, h.slot[0] + (i - 1), j);
+    if (h.nb[1] && i <= d.nx && i > d.nx - h.depth[1]) put(1, h.slot[1] - (d.nx - i), j);
+    if (h.nb[2] && j >= 1 && j <= h.depth[2]) put(2, i, h.slot[2] + (j - 1));
+    if (h.nb[3] && j <= d.ny && j > d.ny - h.depth[3]) put(3, i, h.slot[3] - (d.ny - j));
+    if ((i == 1 || i == d.nx) && (j == 1 || j == d.ny)) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            if (h.nb[4 + c] && i == ((c & 1) ? d.nx : 1) && j == ((c & 2) ? d.ny : 1))
+                put(4 + c, h.cslot[c][0], h.cslot[c][1]);
     }
+}
+
+// A work unit (columns i0 .. i0+w-1, rows ja .. jb) reads halo slots or pushes
+// into a neighbour iff it touches the two cells next to a face.
+__device__ __forceinline__ int rim_unit(const Dom& d, int i0, int w, int ja, int jb) {
+    return (i0 <= 2 || i0 + w - 1 >= d.nx - 1 || ja <= 2 || jb >= d.ny - 1) ? 1 : 0;
 }
 
 // Called by ONE thread per CTA after a barrier over the CTA's working
@@ -197,12 +222,19 @@ __device__ __forceinline__ void halo_signal(const Halo& h) {
     __threadfence_system();
     if (atomicAdd(h.done, 1) == (int)gridDim.x - 1) {
         __threadfence_system();
-        for (int d = 0; d < 4; ++d)
-            if (h.nb[d]) st_release_sys(&h.nb_flags[d][d ^ 1], (unsigned long long)(h.step + 1));
+        for (int q = 0; q < kNbrs; ++q)
+            if (h.nb[q]) st_release_sys(&h.nb_flags[q][opp_dir(q)], (unsigned long long)(h.step + 1));
         *h.done = 0;
         __threadfence();
     }
 }
+
+// The neighbours' 2D fields (sf, pb): static, pushed once after init / upload.
+struct Halo2D {
+    double* sf[kNbrs];
+    double* pb[kNbrs];
+    long long s2j[kNbrs];
+};
 
 //------------------------------------------------------------------------------
 // FUSED_CELL: one owned cell per thread, fastest storage dimension first.
@@ -245,44 +277,35 @@ __global__ void __launch_bounds__(256) step_cell_kernel(const double* __restrict
     }
 }
 
-// Initial / post-upload halo fill: push the current field's faces and the
-// static sf/pb faces into the neighbours' slots (host brackets it with barriers).
+// Initial / post-upload halo fill: push the current field's owned cells and
+// the static sf/pb values near the faces into the neighbours' halo slots with
+// the step kernels' rules (host brackets it with barriers).  A sweep over the
+// owned cells; only those near a face store anything.
 __global__ void exchange_kernel(const double* __restrict__ e, const double* __restrict__ sf,
-                                const double* __restrict__ pb, Dom d, Halo h,
-                                double* nsf0, double* nsf1, double* nsf2, double* nsf3,
-                                double* npb0, double* npb1, double* npb2, double* npb3,
-                                long long n2j0, long long n2j1, long long n2j2, long long n2j3,
-                                int j0, int j1) {
-    double* nsf[4] = {nsf0, nsf1, nsf2, nsf3};
-    double* npb[4] = {npb0, npb1, npb2, npb3};
-    const long long n2j[4] = {n2j0, n2j1, n2j2, n2j3};
-    const long long nj = j1 - j0 + 1;                 // W/E face length (owned j range)
-    const long long ncol = nj * d.nz, nrow = (long long)d.nx * d.nz;
-    const long long n = 2 * ncol + 2 * nrow;
+                                const double* __restrict__ pb, Dom d, Halo h, Halo2D h2) {
+    const Owned o = owned(d);
+    const long long ni = o.i1 - o.i0 + 1, nj = o.j1 - o.j0 + 1;
+    const long long n = ni * nj * d.nz;
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
          t += (long long)gridDim.x * blockDim.x) {
-        int dir, i, j, k;
-        if (t < 2 * ncol) {
-            dir = (int)(t / ncol);
-            const long long r = t % ncol;
-            j = j0 + (int)(r % nj);
-            k = 1 + (int)(r / nj);
-            i = dir == 0 ? 1 : d.nx;
-        } else {
-            const long long q = t - 2 * ncol;
-            dir = 2 + (int)(q / nrow);
-            const long long r = q % nrow;
-            i = 1 + (int)(r % d.nx);
-            k = 1 + (int)(r / d.nx);
-            j = dir == 2 ? 1 : d.ny;
-        }
-        if (!h.nb[dir]) continue;
-        const double v = e[i * d.si + j * d.sj + (long long)(k - 1) * d.sk];
-        const long long ti = dir < 2 ? h.slot[dir] : i, tj = dir < 2 ? j : h.slot[dir];
-        h.nb[dir][ti * h.nsi[dir] + tj * h.nsj[dir] + (long long)(k - 1) * h.nsk[dir]] = v;
+        const int i = o.i0 + (int)(t % ni);
+        const long long r = t / ni;
+        const int j = o.j0 + (int)(r % nj);
+        const int k = 1 + (int)(r / nj);
+        const bool near_i = i <= 2 || i >= d.nx - 1, near_j = j <= 2 || j >= d.ny - 1;
+        if (!near_i && !near_j) continue;
+        halo_push(h, d, i, j, k, e[i * d.si + j * d.sj + (long long)(k - 1) * d.sk]);
         if (k == 1) {
-            nsf[dir][ti + tj * n2j[dir]] = sf[i + j * d.s2j];
-            npb[dir][ti + tj * n2j[dir]] = pb[i + j * d.s2j];
+            // the same targets with 2D strides (k = 1 of a 2D field)
+            Halo hs = h, hp = h;
+            for (int q = 0; q < kNbrs; ++q) {
+                hs.nb[q] = h2.sf[q];
+                hp.nb[q] = h2.pb[q];
+                hs.nsi[q] = hp.nsi[q] = 1;
+                hs.nsj[q] = hp.nsj[q] = h2.s2j[q];
+            }
+            halo_push(hs, d, i, j, 1, sf[i + j * d.s2j]);
+            halo_push(hp, d, i, j, 1, pb[i + j * d.s2j]);
         }
     }
 }
@@ -796,8 +819,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
                     ic = KIJ ? 1 + st * TX : a.fp + 1 + st * TX - 2;
                     // a unit on the subdomain rim reads halo slots and pushes
                     // to that neighbour: wait until it finished the previous step
-                    const int mask = (st == 0 ? 1 : 0) | (st == a.nstrips - 1 ? 2 : 0) |
-                                     (ch == 0 ? 4 : 0) | (ch == a.nchunks - 1 ? 8 : 0);
+                    const int mask = rim_unit(d, 1 + st * TX, TX, ja, jb);
                     if (h.active && mask) {
                         halo_wait(h, mask);
                         asm volatile("fence.proxy.async.global;" ::: "memory");

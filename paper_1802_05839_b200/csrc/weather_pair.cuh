@@ -34,6 +34,18 @@
 // nx+1 and rows 0, 1, ny, ny+1) to small global buffers, and the second of the
 // two units that produce them (strip 0 / last strip of a chunk, chunk 0 / last
 // chunk of a strip) computes those ghost cells -- no grid-wide barrier.
+//
+// Decomposed rank (PairArgs::dist): the same kernel on the
+// rank's subdomain.  A non-owned side's row / column 0 and n+1 are halo cells
+// computed with the inner rule from 2-deep halos (the neighbours pushed them,
+// weather_kernels.cuh); the cyclic partner of an owned ghost intermediate is
+// the far slot (wfar / efar / sfar / nfar) the wrap partner fills.  Units on the
+// rim wait for every neighbour's previous pass and push their cells near a
+// face into the neighbours.  Ghost FINALS need the wrap partner's
+// intermediates, so they move to pair_ghost_kernel: this kernel publishes the
+// ghost-adjacent intermediates and releases a "published" flag in the wrap
+// partners; the ghost kernel waits for theirs, finishes the ghost cells, pushes
+// them and releases the pass to all neighbours.
 #pragma once
 
 #include "weather_kernels.cuh"
@@ -105,11 +117,23 @@ __host__ __device__ inline void pair_rows(const PairArgs& a, int ny, int ch, int
     if (jb > ny) jb = ny;
 }
 
-// Which cyclic partner column a unit's far TMA box holds (0 = none).
-__host__ __device__ inline int pair_far_col(int st, int nstrips, int nx) {
+// Which cyclic partner column a unit's far TMA box holds (0 = none): the
+// partner of an owned i-ghost (wfar for i = 0, efar for i = nx+1) when it lies
+// outside the unit's slab (i0-2 .. i0+TX+1).  Decomposed along i, the partner
+// is the far halo slot -1 / nx+2, always inside the edge strip's slab.
+__host__ __device__ inline bool pair_in_slab(int col, int i0) {
+    return col >= i0 - 2 && col <= i0 + kPairTX + 1;
+}
+template <bool DIST>
+__host__ __device__ inline int pair_far_col(int st, int nstrips, const Dom& d) {
     const int i0 = 1 + st * kPairTX;
-    if (st == 0 && nx > i0 + kPairTX + 1) return nx; // i-ghost 0 needs column nx
-    if (st == nstrips - 1 && st > 0) return 1;       // i-ghost nx+1 needs column 1
+    if (!DIST) { // one domain: wfar = nx, efar = 1
+        if (st == 0 && d.nx > i0 + kPairTX + 1) return d.nx;
+        if (st == nstrips - 1 && st > 0) return 1;
+        return 0;
+    }
+    if (st == 0 && d.own_w && !pair_in_slab(d.wfar, i0)) return d.wfar;
+    if (st == nstrips - 1 && d.own_e && !pair_in_slab(d.efar, i0)) return d.efar;
     return 0;
 }
 
@@ -224,7 +248,7 @@ __device__ __forceinline__ void inter_generic(const IRow& r, double* out, double
 // in the reference's precedence (i ghosts first, weather.cpp:161-168, then j
 // ghosts, :152-159).  The cyclic partner comes from the slab, the far column
 // (fcol/fsp, element fsel) or -- for j ghosts -- global memory.
-template <int KP>
+template <int KP, bool DIST>
 __device__ __forceinline__ void inter_ghost(const IRow& r, double* out, double* ib, int kl, int nk,
                                             int gi, int jr, int cc, int i0, const Dom& d,
                                          const double* __restrict__ e,
@@ -238,15 +262,21 @@ __device__ __forceinline__ void inter_ghost(const IRow& r, double* out, double* 
     const double* e0b = r.e0 - cc; // slab row jr at slab column 0
     const double* s0b = r.S0 - cc;
     const double* b0b = B0 - cc;
-    const bool ig = gi == 0 || gi == nx + 1;
-    const int c1 = 1 - (i0 - 2), cn = nx - (i0 - 2); // slab columns of i = 1 and i = nx
+    const bool ig = DIST ? (d.own_w && gi == 0) || (d.own_e && gi == nx + 1)
+                         : gi == 0 || gi == nx + 1;
+    // i ghosts: u = c2 P(gi) + dv (P(1) + P(nx)) with the partner (the far column
+    // wfar / efar) in the slab or in the far box; weather.cpp:164-167
+    const int ca = gi == 0 || !DIST ? 1 : d.efar, cb = gi == 0 && DIST ? d.wfar : nx;
+    const int c1 = ca - (i0 - 2), cn = cb - (i0 - 2); // their slab columns
     const bool in1 = c1 >= 0 && c1 < W, inn = cn >= 0 && cn < W;
-    const int jf = jr == 0 ? ny : 1; // j ghosts: the partner row, from global memory
+    // j ghosts: the partner row (far row sfar / nfar), from global memory (written
+    // by the wrap partner when decomposed: coherent loads)
+    const int jf = DIST ? (jr == 0 ? d.sfar : d.nfar) : (jr == 0 ? ny : 1);
     const double* ef = e + gi * d.si + jf * d.sj;
     double sff = 0.0, pbf = 0.0;
     if (!ig) {
-        sff = __ldg(sf + gi + jf * d.s2j);
-        pbf = __ldg(pb + gi + jf * d.s2j);
+        sff = DIST ? __ldcg(sf + gi + jf * d.s2j) : __ldg(sf + gi + jf * d.s2j);
+        pbf = DIST ? __ldcg(pb + gi + jf * d.s2j) : __ldg(pb + gi + jf * d.s2j);
     }
 #pragma unroll
     for (int kk = 0; kk < KP; ++kk) {
@@ -260,7 +290,8 @@ __device__ __forceinline__ void inter_ghost(const IRow& r, double* out, double* 
             a = in1 ? Pfull(e0b[o + c1], k, nz, s0b[c1], b0b[c1], ri, tv) : pf; // P(1)
             b = inn ? Pfull(e0b[o + cn], k, nz, s0b[cn], b0b[cn], ri, tv) : pf; // P(nx)
         } else {
-            const double pf = Pfull(__ldg(ef + (long long)(k - 1) * d.sk), k, nz, sff, pbf, ri, tv);
+            const double* pe = ef + (long long)(k - 1) * d.sk;
+            const double pf = Pfull(DIST ? __ldcg(pe) : __ldg(pe), k, nz, sff, pbf, ri, tv);
             // jr = 0: P(ny) far, P(1) = row jr+1; jr = ny+1: P(ny) = row jr-1, P(1) far
             a = jr == 0 ? pf : Pfull(r.em[o], k, nz, r.Sm[0], r.Sm[W], ri, tv);
             b = jr == 0 ? Pfull(r.ep[o], k, nz, r.Sp[0], r.Sp[W], ri, tv) : pf;
@@ -277,10 +308,12 @@ __device__ __forceinline__ void inter_ghost(const IRow& r, double* out, double* 
 // neighbours and the j+1 neighbour from registers (Pc = row j, Pn = row j+1,
 // both this thread's column); only the k neighbours across the group's ends
 // come from B0.  weather.cpp:130-150 on P'.
+// hp (decomposed rim units): push the new cells near a face to the neighbours.
 template <int NK, bool FIRST, bool LAST>
 __device__ __forceinline__ void final_smem(const double* Bm, const double* B0, const double* Pc,
                                            const double* Pn, double* q, long long sk, int kl,
-                                           bool store, const Dom& d) {
+                                           bool store, const Dom& d, const Halo* hp, int gi,
+                                           int j) {
     const double dv = d.dv, c6 = d.c6, c5 = d.c5;
     const int o0 = (kl - 1) * kPairIC;
     Bm += o0;
@@ -302,12 +335,17 @@ __device__ __forceinline__ void final_smem(const double* Bm, const double* B0, c
 #pragma unroll
         for (int kk = 0; kk < NK; ++kk) q[(long long)kk * sk] = v[kk];
     }
+    if (hp) {
+#pragma unroll
+        for (int kk = 0; kk < NK; ++kk) halo_push(*hp, d, gi, j, kl + kk, v[kk]);
+    }
 }
 
 template <int KP>
 __device__ __forceinline__ void final_smem_generic(const double* Bm, const double* B0,
                                                    const double* Bp, double* q, long long sk,
-                                                   int kl, int nk, const Dom& d) {
+                                                   int kl, int nk, const Dom& d, const Halo* hp,
+                                                   int gi, int j) {
     const int nz = d.nz;
     const double dv = d.dv;
 #pragma unroll
@@ -323,6 +361,7 @@ __device__ __forceinline__ void final_smem_generic(const double* Bm, const doubl
         else if (k == nz) v = dadd(dmul(d.c5, B0[o]), dmul(dv, dadd(s, B0[o - kPairIC])));
         else v = dadd(dmul(d.c6, B0[o]), dmul(dv, dadd(dadd(s, B0[o - kPairIC]), B0[o + kPairIC])));
         q[(long long)kk * sk] = v;
+        if (hp) halo_push(*hp, d, gi, j, k, v);
     }
 }
 
@@ -398,11 +437,13 @@ struct PairProducer {
     int slot;  // ring slot of the next load
 };
 
+template <bool DIST>
 __device__ __forceinline__ void pair_issue(PairProducer& p, unsigned char* smem, const PairGeom& G,
                                         uint64_t* full, int* slot_unit, int ns,
                                         const CUtensorMap* tm_e, const CUtensorMap* tm_sfpb,
                                         const CUtensorMap* tm_ef, const CUtensorMap* tm_sfpbf,
-                                        const PairArgs& a, int nx, int ny) {
+                                        const PairArgs& a, const Dom& d, const Halo& h) {
+    const int ny = d.ny;
     if (p.unit < 0) return; // the sentinel is out: nothing left
     const int slot = p.slot;
     p.slot = slot + 1 == ns ? 0 : slot + 1;
@@ -419,10 +460,16 @@ __device__ __forceinline__ void pair_issue(PairProducer& p, unsigned char* smem,
         int ja;
         pair_rows(a, ny, ch, ja, p.jb);
         p.row = ja - 2;
+        if (DIST && rim_unit(d, 1 + (p.unit % a.nstrips) * kPairTX, kPairTX, ja, p.jb)) {
+            // decomposed: the unit reads halo slots the neighbours filled in their
+            // previous pass and pushes into slots they read then
+            halo_wait(h, 1);
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
     }
     const int st = p.unit % a.nstrips;
     const int ic = a.fp + 1 + st * kPairTX - 2; // tensor i of i0 - 2 (even)
-    const int far = pair_far_col(st, a.nstrips, nx);
+    const int far = pair_far_col<DIST>(st, a.nstrips, d);
     slot_unit[slot] = p.unit;
     unsigned char* stg = smem + (size_t)slot * G.stage;
     mbar_expect_tx(&full[slot], far ? G.tx_far : G.tx_main);
@@ -446,15 +493,17 @@ struct RingPos {
     }
 };
 
-// KPT: max k planes per thread (nz <= 8 * KPT).
-template <int KPT>
+// KPT: max k planes per thread (nz <= 8 * KPT).  DIST: a decomposed rank's
+// subdomain (a separate instantiation: the single-domain code is unchanged).
+template <int KPT, bool DIST>
 __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
     step_pair_kernel(const __grid_constant__ CUtensorMap tm_e,
                      const __grid_constant__ CUtensorMap tm_sfpb,
                      const __grid_constant__ CUtensorMap tm_ef,
                      const __grid_constant__ CUtensorMap tm_sfpbf, const double* __restrict__ e,
                      double* __restrict__ u, const double* __restrict__ sf,
-                     const double* __restrict__ pb, Dom d, PairArgs a) {
+                     const double* __restrict__ pb, Dom d, PairArgs a,
+                     const __grid_constant__ Halo h) {
     extern __shared__ __align__(128) unsigned char smem[];
     const PairGeom G = pair_geom(d.nz);
     const int NS = a.ns;
@@ -473,8 +522,8 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
         for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (int s = 0; s < NS; ++s)
-            pair_issue(prod, smem, G, full, slot_unit, NS, &tm_e, &tm_sfpb, &tm_ef, &tm_sfpbf, a,
-                       nx, ny);
+            pair_issue<DIST>(prod, smem, G, full, slot_unit, NS, &tm_e, &tm_sfpb, &tm_ef,
+                             &tm_sfpbf, a, d, h);
     }
     __syncthreads();
 
@@ -517,15 +566,22 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
         const int i0 = 1 + st * kPairTX;
         const int gi = i0 - 2 + cc; // logical i of my intermediate column
         const bool indom = gi <= nx + 1 && nk > 0;
-        const bool owns_i = (gi >= i0 && gi <= min(i0 + kPairTX - 1, nx + 1)) ||
-                            (st == 0 && gi == 0) || (st == a.nstrips - 1 && gi == nx + 1);
-        const bool ig = gi == 0 || gi == nx + 1;
+        // owned columns of this unit (a decomposed rank owns column 0 / nx+1 only
+        // on the global edge; elsewhere they are halo cells)
+        const int ilo = st == 0 ? (!DIST || d.own_w ? 0 : 1) : i0;
+        const int ihi = st == a.nstrips - 1 ? (!DIST || d.own_e ? nx + 1 : nx) : i0 + kPairTX - 1;
+        const bool owns_i = gi >= ilo && gi <= ihi;
+        const bool ig = DIST ? (d.own_w && gi == 0) || (d.own_e && gi == nx + 1)
+                             : gi == 0 || gi == nx + 1;
         // does this thread ever publish in this unit (a ghost-adjacent column, or
         // an inner column whose rows 0, 1, ny, ny+1 may fall in this unit)?
         const bool pub_col = owns_i && (gi <= 1 || gi >= nx);
         const bool pub_row = owns_i && gi >= 1 && gi <= nx && (ja <= 2 || jb >= ny - 1);
-        const int fsel = (a.fp + pair_far_col(st, a.nstrips, nx)) & 1;
+        const int fsel = (a.fp + pair_far_col<DIST>(st, a.nstrips, d)) & 1;
         const bool do_final = cc >= 2 && cc <= kPairTX + 1 && gi <= nx && nk > 0;
+        // decomposed rim unit: final cells within two of a face go to the neighbours
+        const bool rim = DIST && rim_unit(d, i0, kPairTX, ja, jb);
+        const bool push_i = rim && (gi <= 2 || gi >= nx - 1);
         RingPos Ra = R0;          // slab jr-1
         RingPos Rb = Ra.next(NS); // slab jr
         RingPos Rc = Rb.next(NS); // slab jr+1
@@ -551,7 +607,8 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
                              reinterpret_cast<const double*>(sm_ + G.slab),
                              reinterpret_cast<const double*>(s0_ + G.slab),
                              reinterpret_cast<const double*>(sp_ + G.slab)};
-                const bool ghost = ig || jr == 0 || jr == ny + 1;
+                const bool ghost = DIST ? ig || (d.own_s && jr == 0) || (d.own_n && jr == ny + 1)
+                                        : ig || jr == 0 || jr == ny + 1;
                 switch (ghost ? 16 : shape) {
                 case 0: inter_inner<KPT, KPT, false, false>(r, PW2, ibrow, kl, d); break;
                 case 4: inter_inner<KPT, KPT - 1, false, false>(r, PW2, ibrow, kl, d); break;
@@ -563,7 +620,7 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
                         const double* fb = reinterpret_cast<const double*>(sb + G.slab + G.sfpb);
                         const double* fsp =
                             reinterpret_cast<const double*>(sb + G.slab + G.sfpb + G.fcol);
-                        inter_ghost<KPT>(r, PW2, ibrow, kl, nk, gi, jr, cc, i0, d, e, sf, pb, fb,
+                        inter_ghost<KPT, DIST>(r, PW2, ibrow, kl, nk, gi, jr, cc, i0, d, e, sf, pb, fb,
                                          fsp, fsel);
                     } else {
                         inter_generic<KPT>(r, PW2, ibrow, kl, nk, d);
@@ -571,7 +628,9 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
                     break;
                 }
                 if (pub_col || pub_row) {
-                    const bool owns_j = (jr >= ja && jr <= jb) || jr == 0 || jr == ny + 1;
+                    const bool owns_j = (jr >= ja && jr <= jb) ||
+                                        (DIST ? (d.own_s && jr == 0) || (d.own_n && jr == ny + 1)
+                                              : jr == 0 || jr == ny + 1);
                     if (owns_j) pair_publish<KPT>(PW2, kl, nk, gi, jr, d, a);
                 }
             }
@@ -580,8 +639,8 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
             if (tid == 0) {
                 const int nfree = jr == jb + 1 ? 3 : 1;
                 for (int f = 0; f < nfree; ++f)
-                    pair_issue(prod, smem, G, full, slot_unit, NS, &tm_e, &tm_sfpb, &tm_ef,
-                               &tm_sfpbf, a, nx, ny);
+                    pair_issue<DIST>(prod, smem, G, full, slot_unit, NS, &tm_e, &tm_sfpb,
+                                     &tm_ef, &tm_sfpbf, a, d, h);
             }
             if (do_final && jr >= ja + 1) {
                 // row j = jr-1 of e_{s+2} from intermediate rows jr-2, jr-1, jr
@@ -589,12 +648,15 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
                 const double* B0 = ib0 + ib1 * ibn + (cc - 1);
                 const double* Bp = ib0 + ibi * ibn + (cc - 1);
                 double* q = qrow;
+                const int j = jr - 1;
+                const Halo* hp =
+                    DIST && (push_i || (rim && (j <= 2 || j >= ny - 1))) ? &h : nullptr;
                 switch (shape) {
-                case 0: final_smem<KPT, false, false>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d); break;
-                case 4: final_smem<KPT - 1, false, false>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d); break;
-                case 5: final_smem<KPT - 1, true, false>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d); break;
-                case 6: final_smem<KPT - 1, false, true>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d); break;
-                default: final_smem_generic<KPT>(Bm, B0, Bp, q, d.sk, kl, nk, d); break;
+                case 0: final_smem<KPT, false, false>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d, hp, gi, j); break;
+                case 4: final_smem<KPT - 1, false, false>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d, hp, gi, j); break;
+                case 5: final_smem<KPT - 1, true, false>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d, hp, gi, j); break;
+                case 6: final_smem<KPT - 1, false, true>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d, hp, gi, j); break;
+                default: final_smem_generic<KPT>(Bm, B0, Bp, q, d.sk, kl, nk, d, hp, gi, j); break;
                 }
             }
             // No second barrier: the next row's target buffer (ib2) is read here only
@@ -614,9 +676,10 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
         }
         R0 = Rc; // slabs jb+1, jb+2 were Ra, Rb: the next unit starts after them
         // rim units: count the ghost producers; the second one computes the ghosts
+        // (decomposed: pair_ghost_kernel, after the wrap partners published)
         const int inc_c = (st == 0) + (st == a.nstrips - 1);
         const int inc_r = (ch == 0) + (ch == a.nchunks - 1);
-        if (inc_c | inc_r) {
+        if (!DIST && (inc_c | inc_r)) {
             if (tid == 0) {
                 __threadfence();
                 int f = 0;
@@ -638,15 +701,106 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
             __syncthreads(); // s_flags is reused by the next rim unit
         }
     }
-    // the last CTA to finish re-arms the scheduler for the next launch
+    // the last CTA to finish re-arms the scheduler for the next launch and,
+    // decomposed, tells the wrap partners that its intermediates are published
+    // (value = the step after this pass, h.step + 2)
     if (tid == 0) {
-        __threadfence();
+        if (DIST) __threadfence_system();
+        else __threadfence();
         if (atomicAdd(&a.sched[1], 1) == (int)gridDim.x - 1) {
             a.sched[0] = 0;
             a.sched[1] = 0;
+            if (DIST) {
+                __threadfence_system();
+                for (int q = 0; q < 4; ++q)
+                    if (h.nb[q] && h.depth[q] == 1)
+                        st_release_sys(&h.nb_flags[q][kPubFlag + opp_dir(q)],
+                                       (unsigned long long)(h.step + 2));
+            }
             __threadfence();
         }
     }
+}
+
+// Ghost cells of e_{s+2} on a decomposed rank (weather.cpp:152-168 on the
+// intermediate field P'): the i-ghost column of an owned W / E edge (rows of
+// the rank, corners included: the i rule wins) and the j-ghost row of an owned
+// S / N edge (inner columns), from this rank's published P' and the wrap
+// partner's (P2P reads of its gcol / grow; the rank itself when the
+// decomposition has one rank along that axis).  Then every new ghost cell near
+// a face goes to the neighbours, and the last CTA releases the pass (h.step+1
+// = s+2) to all neighbours.
+struct PairGhostArgs {
+    const double* gcol;   // this rank's P' columns 0, 1, nx, nx+1: [4][ny+2][nz]
+    const double* grow;   // this rank's P' rows 0, 1, ny, ny+1: [4][nz][nx+2]
+    const double* gcol_w; // W wrap partner's (its column nx is global nx)
+    const double* gcol_e; // E wrap partner's (its column 1 is global 1)
+    const double* grow_s; // S wrap partner's (its row ny is global ny)
+    const double* grow_n; // N wrap partner's (its row 1 is global 1)
+    int wait[4];          // wait for the wrap partner's "published" flag (W E S N)
+    long long pub;        // the value it releases (s + 2)
+};
+
+__global__ void __launch_bounds__(256) pair_ghost_kernel(double* __restrict__ u, Dom d, Halo h,
+                                                         PairGhostArgs g) {
+    const int nx = d.nx, ny = d.ny, nz = d.nz;
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < 4; ++q)
+            if (g.wait[q]) wait_flag(&h.my_flags[kPubFlag + q], g.pub);
+    }
+    __syncthreads();
+    const Owned o = owned(d);
+    const long long nr = o.j1 - o.j0 + 1;           // owned rows (i-ghost columns)
+    const long long ncol = nr * nz;
+    const long long nw = d.own_w ? ncol : 0, ne = d.own_e ? ncol : 0;
+    const long long nrow = (long long)nx * nz;      // inner columns (j-ghost rows)
+    const long long ns = d.own_s ? nrow : 0, nn = d.own_n ? nrow : 0;
+    const long long n = nw + ne + ns + nn;
+    auto C = [&](const double* b, int w, int j, int k) {
+        return __ldcg(b + ((long long)w * (ny + 2) + j) * nz + (k - 1));
+    };
+    auto R = [&](const double* b, int w, int i, int k) {
+        return __ldcg(b + ((long long)w * nz + (k - 1)) * (nx + 2) + i);
+    };
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < n;
+         t += (long long)gridDim.x * blockDim.x) {
+        int i, j, k;
+        double v;
+        if (t < nw + ne) {
+            const bool west = t < nw;
+            const long long q = west ? t : t - nw;
+            j = o.j0 + (int)(q % nr);
+            k = 1 + (int)(q / nr);
+            if (west) { // (1-2dv) P'(0) + dv (P'(1) + P'(gnx))
+                i = 0;
+                v = dadd(dmul(d.c2, C(g.gcol, 0, j, k)),
+                         dmul(d.dv, dadd(C(g.gcol, 1, j, k), C(g.gcol_w, 2, j, k))));
+            } else {    // (1-2dv) P'(nx+1) + dv (P'(1) + P'(nx))
+                i = nx + 1;
+                v = dadd(dmul(d.c2, C(g.gcol, 3, j, k)),
+                         dmul(d.dv, dadd(C(g.gcol_e, 1, j, k), C(g.gcol, 2, j, k))));
+            }
+        } else {
+            const long long q0 = t - nw - ne;
+            const bool south = q0 < ns;
+            const long long q = south ? q0 : q0 - ns;
+            i = 1 + (int)(q % nx);
+            k = 1 + (int)(q / nx);
+            if (south) { // (1-2dv) P'(j=0) + dv (P'(gny) + P'(1))
+                j = 0;
+                v = dadd(dmul(d.c2, R(g.grow, 0, i, k)),
+                         dmul(d.dv, dadd(R(g.grow_s, 2, i, k), R(g.grow, 1, i, k))));
+            } else {     // (1-2dv) P'(ny+1) + dv (P'(ny) + P'(1))
+                j = ny + 1;
+                v = dadd(dmul(d.c2, R(g.grow, 3, i, k)),
+                         dmul(d.dv, dadd(R(g.grow, 2, i, k), R(g.grow_n, 1, i, k))));
+            }
+        }
+        u[i * d.si + j * d.sj + (long long)(k - 1) * d.sk] = v;
+        halo_push(h, d, i, j, k, v);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) halo_signal(h);
 }
 
 } // namespace hftw

@@ -105,8 +105,8 @@ __device__ __forceinline__ void wave_ghost_cols(const double* __restrict__ e,
                                                 double* __restrict__ u,
                                                 const double* __restrict__ sf,
                                                 const double* __restrict__ pb, const Dom& d,
-                                                int ja, int jb, bool west, bool east, int tid,
-                                                int nthreads) {
+                                                const Halo& h, int ja, int jb, bool west,
+                                                bool east, int tid, int nthreads) {
     const int nr = jb - ja + 1;
     const long long per = (long long)nr * d.nz;
     const long long n = per * ((west ? 1 : 0) + (east ? 1 : 0));
@@ -116,7 +116,9 @@ __device__ __forceinline__ void wave_ghost_cols(const double* __restrict__ e,
         const int j = ja + (int)(q % nr);
         const int k = 1 + (int)(q / nr);
         const int i = w ? 0 : d.nx + 1;
-        u[i * d.si + j * d.sj + (long long)(k - 1) * d.sk] = cell_update<true, true>(e, sf, pb, d, i, j, k);
+        const double v = cell_update<true, true>(e, sf, pb, d, i, j, k);
+        u[i * d.si + j * d.sj + (long long)(k - 1) * d.sk] = v;
+        halo_push(h, d, i, j, k, v); // a ghost column's first / last rows go to S / N
     }
 }
 
@@ -128,8 +130,8 @@ __device__ __forceinline__ void wave_item_done(const WaveArgs& a, int s, int per
     __threadfence_system(); // this item's pushes into the neighbours precede the count
     if (atomicAdd(&a.step_done[s], 1) == per_step - 1) {
         __threadfence_system();
-        for (int dd = 0; dd < 4; ++dd)
-            if (h.nb[dd]) st_release_sys(&h.nb_flags[dd][dd ^ 1], (unsigned long long)(h.step + s + 1));
+        for (int q = 0; q < kNbrs; ++q)
+            if (h.nb[q]) st_release_sys(&h.nb_flags[q][opp_dir(q)], (unsigned long long)(h.step + s + 1));
     }
 }
 
@@ -231,7 +233,7 @@ __device__ __forceinline__ void wave_consumers(unsigned char* smem, const SlabGe
         L = lend + 2;
         // the i-ghost columns of these rows (their partners are in the same rows)
         const bool west = st == 0 && d.own_w, east = st == a.nstrips - 1 && d.own_e;
-        if (west || east) wave_ghost_cols(e, u, sf, pb, d, ja, jb, west, east, tid, nthreads);
+        if (west || east) wave_ghost_cols(e, u, sf, pb, d, hs, ja, jb, west, east, tid, nthreads);
         // publish: every consumer's stores of this unit precede the count
         asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
         if (tid == 0) {
@@ -315,8 +317,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
                     // neighbour pushed in its step s-1 and pushes into slots it read
                     // then -- wait until that neighbour has finished step s-1
                     const Halo& hs = (s & 1) ? a.h_odd : a.h_even;
-                    const int mask = (st == 0 ? 1 : 0) | (st == a.nstrips - 1 ? 2 : 0) |
-                                     (ch == 0 ? 4 : 0) | (ch == last ? 8 : 0);
+                    const int mask = rim_unit(d, 1 + st * TX, TX, ja, jb);
                     if (hs.active && mask) {
                         Halo hw = hs;
                         hw.step = hs.step + s;

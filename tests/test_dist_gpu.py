@@ -78,6 +78,9 @@ def _worker(rank, world, port, shape, grid, steps, layout, kernel, random_init, 
     # multi-step launches with in-kernel pushes and per-step flags, many steps per call
     ((131, 97, 12), (2, 2), 11, "ijk", "fused_tma", True),
     ((200, 140, 20), (2, 4), 9, "ijk", "auto", True),
+    # two-step passes per rank across processes (CUDA IPC: faces, corners, P')
+    ((130, 100, 58), (2, 4), 7, "ijk", "auto", True),
+    ((97, 95, 57), (3, 3), 6, "ijk", "auto", False),
 ])
 def test_decomposed_gpu_bitwise(shape, grid, steps, layout, kernel, random_init):
     _run_decomposed(shape, grid, steps, layout, kernel, random_init)

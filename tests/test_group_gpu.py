@@ -48,6 +48,16 @@ def assert_bitwise(got, want, tag):
     ((97, 61, 13), (3, 1), [2, 3], "ijk", "auto"),
     ((100, 70, 9), (3, 2), [3, 2], "ijk", "auto"),
     ((40, 30, 8), (1, 1), [4], "ijk", "auto"),
+    # two-step passes on every rank (AUTO with 56 <= nz <= 58): 2-deep halos,
+    # diagonal corner columns, ghost finals from the wrap partners' P'
+    ((150, 97, 58), (2, 2), [5, 3], "ijk", "auto"),
+    ((130, 100, 58), (2, 4), [7], "ijk", "auto"),
+    ((160, 61, 56), (4, 2), [6], "ijk", "auto"),
+    ((97, 95, 57), (3, 3), [4, 5], "ijk", "auto"),
+    ((70, 130, 58), (1, 3), [5], "ijk", "auto"),
+    ((90, 64, 58), (3, 1), [6, 2], "ijk", "auto"),
+    ((120, 90, 20), (2, 2), [5], "ijk", "fused_pair"),   # generic row shapes
+    ((64, 40, 58), (8, 1), [3], "ijk", "auto"),          # 8-column ranks
 ])
 def test_group_random_state_bitwise(coracle, shape, grid, calls, layout, kernel):
     nx, ny, nz = shape
