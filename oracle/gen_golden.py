@@ -127,6 +127,20 @@ def main():
             variants[f"{name}{'-reverse' if rev else ''}"] = {
                 "max_line_length": mll or 132, "bitwise_equal_to_reference": bool(same)}
 
+    #     ... and at the DEFAULT max_line_length (132), where the reference's own
+    #     run_variant cannot run the emitted-code variants (its split lands inside
+    #     macro invocations; gpu-emulated crashes): the expand-first oracle
+    #     (ref_capi.cpp)
+    for v, name in [(2, "cpu"), (3, "gpu-emulated")]:
+        for rev in (False, True):
+            s, msg = ref.run_variant_expand_first(v, g, 10, 132, rev)
+            same = s is not None and all(np.array_equal(a, b) for a, b in
+                                         zip(s.fields().values(), nat.fields().values()))
+            variants[f"{name}{'-reverse' if rev else ''}@132-expand-first"] = {
+                "max_line_length": 132, "bitwise_equal_to_reference": bool(same),
+                "write_data_calls": ref.last_write_calls,
+                "fnv1a64": {k: c.fnv(a) for k, a in s.fields().items()} if s else None}
+
     # (8) the corpus driver's output cadence (simple_weather.h90:91-95): number
     #     of write_data calls of the interpreted original for (steps, dt, out_dt)
     writes = []

@@ -169,6 +169,7 @@ class RefOracle:
         L.hftref_run_variant.argtypes = [C.c_int, C.POINTER(Grid), C.c_longlong, C.c_int,
                                          C.c_int, C.c_char_p, D, D, D, D, C.c_char_p,
                                          C.c_size_t, C.POINTER(C.c_int)]
+        L.hftref_run_variant_expand_first.argtypes = L.hftref_run_variant.argtypes
         LL = C.POINTER(C.c_longlong)
         L.hftref_compare_arrays.argtypes = [C.c_int, LL, LL, D, D, D, D, LL]
         L.hftref_unpermute.argtypes = [C.c_int, LL, LL, C.POINTER(C.c_int), D, D, LL, LL]
@@ -207,6 +208,22 @@ class RefOracle:
                                          corpus_dir.encode(), _p(s.energy), _p(s.energy_u),
                                          _p(s.energy_surf), _p(s.energy_pbl), buf, 1 << 16,
                                          C.byref(wc))
+        self.last_write_calls = wc.value
+        return (s if ok else None), buf.value.decode()
+
+    def run_variant_expand_first(self, variant: int, g: Grid, n: int,
+                                 max_line_length: int = 132, reverse: bool = False,
+                                 corpus_dir: str = CORPUS_DIR):
+        """The emitted-code variants (2 = cpu, 3 = gpu-emulated) with the storage
+        macros expanded BEFORE the line split (ref_capi.cpp): runs at the default
+        max_line_length, where hft::run_variant fails (SURVEY.md 8(f) item 3)."""
+        s = empty_state(g)
+        buf = C.create_string_buffer(1 << 16)
+        wc = C.c_int(0)
+        ok = self.lib.hftref_run_variant_expand_first(
+            variant, C.byref(g), n, max_line_length, int(reverse), corpus_dir.encode(),
+            _p(s.energy), _p(s.energy_u), _p(s.energy_surf), _p(s.energy_pbl), buf, 1 << 16,
+            C.byref(wc))
         self.last_write_calls = wc.value
         return (s if ok else None), buf.value.decode()
 

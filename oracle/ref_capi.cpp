@@ -15,6 +15,9 @@
 #include <vector>
 
 #include "hft/config.hpp"
+#include "hft/interpreter.hpp"
+#include "hft/lines.hpp"
+#include "hft/parser.hpp"
 #include "hft/pipeline.hpp"
 #include "hft/weather.hpp"
 
@@ -127,6 +130,88 @@ int hftref_run_variant(int variant, const Grid* g, long long steps, int max_line
     if (!r.ok) return 0;
     put_state(r.state, e, eu, sf, pb);
     return 1;
+}
+
+// the emitted-code variants (cpu / gpu-emulated) at the
+// DEFAULT max_line_length.  The reference splits long lines at transpile time
+// (pipeline.cpp:88) and expands the storage macros on the consumer side
+// afterwards (pipeline.cpp:103-113, run_units at weather.cpp:401-437), so a
+// split can land inside a macro invocation and run_variant(GpuEmulated) fails
+// below max_line_length 268.  This oracle uses only the reference's own phases
+// in the order that works: transpile without a line limit, expand each unit,
+// THEN split the plain text at `max_line_length`, re-merge and interpret.  The
+// driver (initialize, then simulate(0, (steps - 0.5) dt, dt, out_dt)) and the
+// field read-back restate drive() / extract_state() (weather.cpp:364-397),
+// which the reference keeps file-local.  variant: 2 = cpu, 3 = gpu-emulated.
+int hftref_run_variant_expand_first(int variant, const Grid* g, long long steps,
+                                    int max_line_length, int reverse, const char* corpus_dir,
+                                    double* e, double* eu, double* sf, double* pb, char* msg,
+                                    size_t cap, int* write_calls) {
+    hft::Diagnostics d;
+    const hft::GridConfig gc = to_cfg(g);
+    std::vector<hft::LoadedSource> srcs;
+    for (const char* f : {"simple_weather.h90", "physics.h90", "diffusion.h90"})
+        srcs.push_back(hft::load_and_merge(std::string(corpus_dir) + "/" + f, d));
+    hft::BuildConfig unsplit;
+    unsplit.max_line_length = 1 << 20; // no transpile-time split
+    const bool gpu = variant == 3;
+    hft::TranspileResult tr = hft::transpile(srcs, unsplit, gpu ? "gpu-cuda" : "cpu-openmp", d);
+    std::vector<std::vector<hft::LogicalLine>> files;
+    for (std::size_t n = 1; d.ok() && n < tr.units.size(); ++n) {
+        const std::string text = hft::expand_unit(tr.units[0], tr.units[n], gpu, d);
+        std::vector<std::string> lines;
+        std::string cur;
+        for (char ch : text) {
+            if (ch == '\n') {
+                lines.push_back(cur);
+                cur.clear();
+            } else {
+                cur += ch;
+            }
+        }
+        if (!cur.empty()) lines.push_back(cur);
+        std::string split;
+        for (const auto& l : hft::split_lines(lines, max_line_length, d)) split += l + "\n";
+        const std::string& fn = tr.units[n].filename;
+        hft::LoadedSource ls = hft::prepare_source(fn.substr(0, fn.rfind('.')) + ".h90", split, d);
+        files.push_back(std::move(ls.logical));
+    }
+    int ok = 0;
+    if (d.ok()) {
+        hft::ast::Program prog = hft::parse_program(files, d);
+        hft::InterpreterOptions io;
+        io.emulate_kernels = gpu;
+        io.launch_order = reverse ? hft::LaunchOrder::Reverse : hft::LaunchOrder::Forward;
+        if (d.ok()) {
+            hft::Interpreter it(prog, d, io);
+            int writes = 0;
+            it.on_write_data = [&](const std::string&, double, const hft::ArrayObject&) { ++writes; };
+            it.set_global_int("nx", gc.nx);
+            it.set_global_int("ny", gc.ny);
+            it.set_global_int("nz", gc.nz);
+            const double end_time = (static_cast<double>(steps) - 0.5) * gc.timestep;
+            if (it.call("initialize") &&
+                it.call("simulate", {0.0, end_time, gc.timestep, gc.output_timestep})) {
+                const hft::ast::Arch arch = gpu ? hft::ast::Arch::Gpu : hft::ast::Arch::Cpu;
+                const std::pair<const char*, int> fields[] = {
+                    {"energy", 3}, {"energy_u", 3}, {"energy_surf", 2}, {"energy_pbl", 2}};
+                double* outs[] = {e, eu, sf, pb};
+                ok = 1;
+                for (int f = 0; f < 4; ++f) {
+                    const hft::ArrayObject* raw = it.find_array(fields[f].first);
+                    if (!raw) {
+                        ok = 0;
+                        break;
+                    }
+                    put(hft::unpermute_storage(*raw, unsplit.storage_order(arch, fields[f].second)),
+                        outs[f]);
+                }
+                if (write_calls) *write_calls = writes;
+            }
+        }
+    }
+    copy_msg(d, msg, cap);
+    return ok && d.ok() ? 1 : 0;
 }
 
 // hft::compare_arrays (weather.cpp:184-217) over flat logical buffers of

@@ -115,6 +115,8 @@ struct hftw_ctx {
     size_t staging_n = 0;
     int cur = 0;               // buf[cur] holds SimState::energy
     bool eu_derived = false;   // energy_u == physics(buf[cur ^ 1]), not yet materialised
+    bool eu_stored = false;    // energy_u is in eu_buf (written by the last pair pass)
+    double* eu_buf = nullptr;  // third field buffer (allocated by the first such pass)
 
     // TMA kernel state
     bool tma_ok = false;
@@ -281,6 +283,9 @@ Halo make_halo(const hftw_ctx* c, int dst) {
 }
 
 double* e3(const hftw_ctx* c, int b) { return c->buf[b] + c->off3; }
+// where SimState::energy_u lives: the ping-pong partner, or the third buffer
+// the last pair pass of a call wrote it to
+double* eu_field(const hftw_ctx* c) { return c->eu_stored ? c->eu_buf + c->off3 : e3(c, c->cur ^ 1); }
 double* sf2(const hftw_ctx* c) { return c->sf + c->off2; }
 double* pb2(const hftw_ctx* c) { return c->pb + c->off2; }
 
@@ -468,6 +473,15 @@ int setup_tma(hftw_ctx* c) {
     return HFTW_OK;
 }
 
+using PairKernel = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap,
+                           const CUtensorMap, const double*, double*, const double*,
+                           const double*, Dom, hftw::PairArgs, const Halo);
+PairKernel pair_kernel(bool dist, bool eu) {
+    using hftw::step_pair_kernel;
+    return dist ? (eu ? step_pair_kernel<kPairKPT, true, true> : step_pair_kernel<kPairKPT, true, false>)
+                : (eu ? step_pair_kernel<kPairKPT, false, true> : step_pair_kernel<kPairKPT, false, false>);
+}
+
 // The two-steps-per-pass kernel (weather_pair.cuh): IJK, single domain, nz
 // <= 64 (8 k values per thread), and a >= 4-deep slab ring next to the two
 // intermediate row buffers.  Leaves pair_ok = false otherwise.
@@ -485,8 +499,7 @@ int setup_pair(hftw_ctx* c) {
     int smem_optin = 0;
     CUDA_TRY(c, cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin,
                                        c->device));
-    auto kern = c->dist ? hftw::step_pair_kernel<kPairKPT, true>
-                        : hftw::step_pair_kernel<kPairKPT, false>;
+    auto kern = pair_kernel(c->dist, true); // the largest static footprint of the four
     cudaFuncAttributes fa{};
     CUDA_TRY(c, cudaFuncGetAttributes(&fa, kern));
     const int nz = (int)c->nz;
@@ -505,7 +518,8 @@ int setup_pair(hftw_ctx* c) {
     if (!ns) return HFTW_OK;
     c->pair_ns = ns;
     c->pair_smem = hftw::pair_smem_bytes(nz, ns);
-    CUDA_TRY(c, raise_smem_attr((const void*)kern, c->pair_smem));
+    for (bool eu : {false, true})
+        CUDA_TRY(c, raise_smem_attr((const void*)pair_kernel(c->dist, eu), c->pair_smem));
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, hftw::kPairThreads,
                                                       c->pair_smem) != cudaSuccess ||
@@ -612,7 +626,8 @@ double* gpub_of(double* base, size_t per, long long pass) {
 }
 
 // Two fused steps in one launch: buf[src] -> buf[src ^ 1] = step(step(buf[src])).
-int launch_pair(hftw_ctx* c, int src) {
+// eu: also store the intermediate field's post-physics values as energy_u.
+int launch_pair(hftw_ctx* c, int src, bool eu) {
     Dom d = make_dom(c);
     hftw::PairArgs a{};
     a.fp = kFrontPad;
@@ -632,8 +647,8 @@ int launch_pair(hftw_ctx* c, int src) {
     const Halo h = make_halo(c, src ^ 1); // pushes into the neighbours' e_{s+2}, waits >= s
     int rc = timing_mark(c, 1, true);
     if (rc) return rc;
-    auto kern = c->dist ? hftw::step_pair_kernel<kPairKPT, true>
-                        : hftw::step_pair_kernel<kPairKPT, false>;
+    if (eu) a.eu = c->eu_buf + c->off3;
+    auto kern = pair_kernel(c->dist, eu);
     kern<<<c->pair_ctas, hftw::kPairThreads, c->pair_smem, c->stream>>>(
         c->tm_e2[src], c->tm_sfpb, c->tm_ef[src], c->tm_sfpbf, e3(c, src), e3(c, src ^ 1), sf2(c),
         pb2(c), d, a, h);
@@ -681,22 +696,34 @@ int launch_pair_ghost(hftw_ctx* c, int dst) {
     return HFTW_OK;
 }
 
-// Two-step passes of an n-step call: pairs, then one or two single steps (the
-// last step is a single-step launch so that energy_u, the physics of the field
-// before it, stays derivable from the ping-pong partner).
-int64_t pair_passes(int64_t nsteps) { return nsteps >= 3 ? (nsteps - 1) / 2 : 0; }
+// Two-step passes of an n-step call: n/2 when n is even (the last one also
+// stores energy_u, the intermediate field's post-physics values), else
+// (n-1)/2 and a final single step (energy_u = physics of the field before it
+// stays derivable from the ping-pong partner).
+int64_t pair_passes(int64_t nsteps) { return nsteps / 2; }
 
 // One pass: phase bit 0 launches the pair kernel, bit 1 (decomposed) the ghost
 // kernel, and then the bookkeeping.  A group on one device runs bit 0 for every
 // rank before bit 1 for any (the ghost kernels wait for the wrap partners').
-int pair_pass(hftw_ctx* c, int phase) {
+int pair_pass(hftw_ctx* c, int phase, bool eu) {
     int rc;
-    if ((phase & 1) && (rc = launch_pair(c, c->cur))) return rc;
+    if (phase & 1) {
+        if (eu && !c->eu_buf &&
+            cudaMalloc(&c->eu_buf, c->n3 * sizeof(double)) != cudaSuccess) {
+            cudaGetLastError();
+            c->eu_buf = nullptr;
+            return fail(c, HFTW_ENOMEM, "cudaMalloc of the energy_u buffer (%zu bytes) failed",
+                        c->n3 * sizeof(double));
+        }
+        if ((rc = launch_pair(c, c->cur, eu))) return rc;
+    }
     if (phase & 2) {
         if (c->dist && (rc = launch_pair_ghost(c, c->cur ^ 1))) return rc;
         c->cur ^= 1;
         c->step_count += 2;
         ++c->pass_count;
+        c->eu_stored = eu;
+        c->eu_derived = false;
     }
     return HFTW_OK;
 }
@@ -901,7 +928,7 @@ int launch_physics(hftw_ctx* c, int b, int mode) {
 // in the buffer that holds the previous energy (it is dead until the next step
 // overwrites it, so this is free of hazards; only owned cells are touched).
 int materialize_eu(hftw_ctx* c) {
-    if (!c->eu_derived) return HFTW_OK;
+    if (!c->eu_derived) return HFTW_OK; // materialised, or stored by a pair pass
     int rc = launch_physics(c, c->cur ^ 1, best_physics_mode(c));
     if (rc) return rc;
     c->eu_derived = false;
@@ -1257,7 +1284,7 @@ int group_step(hftw_ctx* c, int64_t nsteps) {
                 for (int phase : {1, 2})
                     for (hftw_ctx* r : c->ranks) {
                         RANK_TRY(c, r, check_ctx(r));
-                        RANK_TRY(c, r, pair_pass(r, phase));
+                        RANK_TRY(c, r, pair_pass(r, phase, nsteps % 2 == 0 && p == pairs - 1));
                     }
             nsteps -= 2 * pairs;
         }
@@ -1470,6 +1497,7 @@ void hftw_destroy(hftw_ctx* c) {
     if (c->d_pair) cudaFree(c->d_pair);
     if (c->d_wave) cudaFree(c->d_wave);
     if (c->gpub) cudaFree(c->gpub);
+    if (c->eu_buf) cudaFree(c->eu_buf);
     for (auto& t : c->tev) {
         cudaEventDestroy(t.a);
         cudaEventDestroy(t.b);
@@ -1517,6 +1545,7 @@ int hftw_init(hftw_ctx* c) {
     if (c->d_sched) CUDA_TRY(c, cudaMemsetAsync(c->d_sched, 0, 2 * sizeof(int), c->stream));
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     c->eu_derived = false; // energy_u is all zeros (weather.cpp:82)
+    c->eu_stored = false;
     c->poisoned = 0;
     if (c->dist) c->halo_dirty = true;
     return HFTW_OK;
@@ -1539,6 +1568,7 @@ int hftw_upload(hftw_ctx* c, int field, const double* host) {
     case HFTW_ENERGY_U:
         rc = copy_3d(c, e3(c, c->cur ^ 1), h, true);
         c->eu_derived = false;
+        c->eu_stored = false;
         break;
     case HFTW_ENERGY_SURF:
     case HFTW_ENERGY_PBL:
@@ -1570,7 +1600,7 @@ int hftw_download(hftw_ctx* c, int field, double* host) {
         break;
     case HFTW_ENERGY_U:
         if ((rc = materialize_eu(c))) return rc;
-        rc = copy_3d(c, e3(c, c->cur ^ 1), host, false);
+        rc = copy_3d(c, eu_field(c), host, false);
         break;
     case HFTW_ENERGY_SURF:
         rc = copy_2d(c, sf2(c), host, false);
@@ -1607,7 +1637,7 @@ int hftw_step(hftw_ctx* c, int64_t nsteps) {
         // derivable from the ping-pong partner
         const int64_t pairs = pair_passes(nsteps);
         for (int64_t p = 0; p < pairs; ++p)
-            if ((rc = pair_pass(c, 3))) return rc;
+            if ((rc = pair_pass(c, 3, nsteps % 2 == 0 && p == pairs - 1))) return rc;
         nsteps -= 2 * pairs;
     }
     const bool multistep = c->opt_multistep > 0 || (c->opt_multistep == 0 && c->wave_pref);
@@ -1624,6 +1654,7 @@ int hftw_step(hftw_ctx* c, int64_t nsteps) {
             if (n & 1) c->cur ^= 1;
             c->step_count += n;
             c->eu_derived = true;
+            c->eu_stored = false;
             nsteps -= n;
         }
     }
@@ -1639,10 +1670,12 @@ int hftw_step(hftw_ctx* c, int64_t nsteps) {
                                                                : HFTW_KERNEL_FUSED_CELL)))
                 return rc;
             c->eu_derived = false;
+            c->eu_stored = false;
         } else {
             if (k1 != HFTW_KERNEL_FUSED_CELL && (rc = timing_mark(c, 0, true))) return rc;
             if ((rc = launch_fused<true>(c, c->cur, k1))) return rc;
             c->eu_derived = true;
+            c->eu_stored = false;
         }
         if ((rc = timing_mark(c, 0, false))) return rc;
         c->cur ^= 1;
@@ -1815,6 +1848,7 @@ int hftw_diffuse(hftw_ctx* c) {
                                   c->tma_ok ? HFTW_KERNEL_FUSED_TMA : HFTW_KERNEL_FUSED_CELL)))
         return rc;
     c->eu_derived = false; // energy_u = the diffused input (swap semantics)
+    c->eu_stored = false;
     c->cur ^= 1;
     return HFTW_OK;
 }
@@ -1858,7 +1892,7 @@ int hftw_field_view(hftw_ctx* c, int field, void** dptr, int64_t strides[3]) {
     if (c->dist) c->halo_dirty = true;
     switch (field) {
     case HFTW_ENERGY: *dptr = e3(c, c->cur); break;
-    case HFTW_ENERGY_U: *dptr = e3(c, c->cur ^ 1); break;
+    case HFTW_ENERGY_U: *dptr = eu_field(c); break;
     case HFTW_ENERGY_SURF: *dptr = sf2(c); break;
     case HFTW_ENERGY_PBL: *dptr = pb2(c); break;
     }
@@ -2217,6 +2251,7 @@ int hftw_step_host(hftw_ctx* c, const double* energy, const double* energy_surf,
         cudaStreamSynchronize(c->stream);
         cudaGetLastError();
         c->eu_derived = false;
+        c->eu_stored = false;
         c->poisoned = 0xF;
     }
     return rc;
@@ -2346,6 +2381,7 @@ int step_host_pipeline(hftw_ctx* c, const double* energy, const double* energy_s
     // the context now holds the stepped state, as after upload x3 + step(1)
     c->cur ^= 1;
     c->eu_derived = true;
+    c->eu_stored = false;
     c->poisoned = 0;
     ++c->step_count;
     return HFTW_OK;

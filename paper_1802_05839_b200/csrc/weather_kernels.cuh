@@ -209,6 +209,18 @@ __device__ __forceinline__ void halo_push(const Halo& h, const Dom& d, int i, in
     }
 }
 
+// Push the column (i, j, kl .. kl+nk-1) that this thread has just stored at src
+// (step src_sk between planes; global memory or a shared staging row) to the
+// neighbours.  Out of line: the hot loops stay small (inlined pushes cost the
+// instruction cache more than the stores), and only cells next to a face call it.
+__device__ __noinline__ void push_column(const Halo& h, const Dom& d, const double* src,
+                                         long long src_sk, int i, int j, int kl, int nk) {
+    for (int kk = 0; kk < nk; ++kk) halo_push(h, d, i, j, kl + kk, src[(long long)kk * src_sk]);
+}
+__device__ __forceinline__ bool near_face(const Dom& d, int i, int j) {
+    return i <= 2 || i >= d.nx - 1 || j <= 2 || j >= d.ny - 1;
+}
+
 // A work unit (columns i0 .. i0+w-1, rows ja .. jb) reads halo slots or pushes
 // into a neighbour iff it touches the two cells next to a face.
 __device__ __forceinline__ int rim_unit(const Dom& d, int i0, int w, int ja, int jb) {
@@ -736,7 +748,6 @@ __device__ __forceinline__ void column_row(const ColumnRow& r, const Halo& h, co
         double pn;
         const double out = edge(k, pd, pc, pn);
         r.up[(long long)(k - r.kl) * r.sk] = out;
-        if (PUSH) halo_push(h, d, r.i, r.j, k, out);
         pd = pc;
         pc = pn;
     }
@@ -756,7 +767,6 @@ __device__ __forceinline__ void column_row(const ColumnRow& r, const Halo& h, co
             s6 = dadd(dadd(s6, pd), pn);
             const double out = dadd(dmul(c6, pc), dmul(dv, s6));
             *q = out;
-            if (PUSH) halo_push(h, d, r.i, r.j, k, out);
             q += r.sk;
             p0 += w;
             pm += w;
@@ -769,10 +779,12 @@ __device__ __forceinline__ void column_row(const ColumnRow& r, const Halo& h, co
         double pn;
         const double out = edge(k, pd, pc, pn);
         r.up[(long long)(k - r.kl) * r.sk] = out;
-        if (PUSH) halo_push(h, d, r.i, r.j, k, out);
         pd = pc;
         pc = pn;
     }
+    // decomposed: the column's cells near a face go to the neighbours (read back
+    // from where this thread just stored them)
+    if (PUSH && near_face(d, r.i, r.j)) push_column(h, d, r.up, r.sk, r.i, r.j, r.kl, r.kh - r.kl + 1);
 }
 
 template <int TX, int NCW, bool PHYS, bool KIJ>
@@ -781,7 +793,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
                     const __grid_constant__ CUtensorMap tm_sf,
                     const __grid_constant__ CUtensorMap tm_pb, const double* __restrict__ e,
                     double* __restrict__ u, const double* __restrict__ sf,
-                    const double* __restrict__ pb, Dom d, TmaArgs a, Halo h) {
+                    const double* __restrict__ pb, Dom d, TmaArgs a,
+                    const __grid_constant__ Halo h) {
     extern __shared__ __align__(128) unsigned char smem[];
     const SlabGeom G = KIJ ? slab_geom_kij(TX, a.pk) : slab_geom(TX, d.nz);
     const int NS = a.ns;

@@ -108,6 +108,8 @@ struct PairArgs {
     int* cnt_row; // [nstrips] j-ghost producers done (chunk 0 + last chunk), self-resetting
     double* gcol; // P' at i = 0, 1, nx, nx+1: [4][ny+2][nz]
     double* grow; // P' at j = 0, 1, ny, ny+1: [4][nz][nx+2]
+    double* eu;   // EU passes: energy_u = P' (the intermediate field, post-physics) of
+                  // every owned cell, at logical (0,0,1) of a third field buffer
 };
 
 // Rows ja..jb of chunk ch.
@@ -335,10 +337,7 @@ __device__ __forceinline__ void final_smem(const double* Bm, const double* B0, c
 #pragma unroll
         for (int kk = 0; kk < NK; ++kk) q[(long long)kk * sk] = v[kk];
     }
-    if (hp) {
-#pragma unroll
-        for (int kk = 0; kk < NK; ++kk) halo_push(*hp, d, gi, j, kl + kk, v[kk]);
-    }
+    if (hp) push_column(*hp, d, q, sk, gi, j, kl, NK);
 }
 
 template <int KP>
@@ -361,8 +360,8 @@ __device__ __forceinline__ void final_smem_generic(const double* Bm, const doubl
         else if (k == nz) v = dadd(dmul(d.c5, B0[o]), dmul(dv, dadd(s, B0[o - kPairIC])));
         else v = dadd(dmul(d.c6, B0[o]), dmul(dv, dadd(dadd(s, B0[o - kPairIC]), B0[o + kPairIC])));
         q[(long long)kk * sk] = v;
-        if (hp) halo_push(*hp, d, gi, j, k, v);
     }
+    if (hp) push_column(*hp, d, q, sk, gi, j, kl, nk);
 }
 
 // Publish the ghost-adjacent intermediates a unit owns (see PairArgs).
@@ -495,7 +494,10 @@ struct RingPos {
 
 // KPT: max k planes per thread (nz <= 8 * KPT).  DIST: a decomposed rank's
 // subdomain (a separate instantiation: the single-domain code is unchanged).
-template <int KPT, bool DIST>
+// EU: the last pass of a call also stores P' as SimState::energy_u (weather.cpp:170
+// makes energy_u the post-physics field of the last step), so a call of n even
+// steps needs no trailing single steps.
+template <int KPT, bool DIST, bool EU>
 __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
     step_pair_kernel(const __grid_constant__ CUtensorMap tm_e,
                      const __grid_constant__ CUtensorMap tm_sfpb,
@@ -627,11 +629,18 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
                     }
                     break;
                 }
-                if (pub_col || pub_row) {
+                if (pub_col || pub_row || EU) {
                     const bool owns_j = (jr >= ja && jr <= jb) ||
                                         (DIST ? (d.own_s && jr == 0) || (d.own_n && jr == ny + 1)
                                               : jr == 0 || jr == ny + 1);
-                    if (owns_j) pair_publish<KPT>(PW2, kl, nk, gi, jr, d, a);
+                    if (owns_j && (pub_col || pub_row)) pair_publish<KPT>(PW2, kl, nk, gi, jr, d, a);
+                    if (EU && owns_j && owns_i) {
+                        double* q = a.eu + (long long)gi * d.si + (long long)jr * d.sj +
+                                    (long long)(kl - 1) * d.sk;
+#pragma unroll
+                        for (int kk = 0; kk < KPT; ++kk)
+                            if (kk < nk) q[(long long)kk * d.sk] = PW2[kk];
+                    }
                 }
             }
             __syncthreads(); // intermediate row jr complete; slab jr-1 free

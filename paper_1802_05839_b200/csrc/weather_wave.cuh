@@ -251,7 +251,8 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
                      const __grid_constant__ CUtensorMap tm_e1,
                      const __grid_constant__ CUtensorMap tm_sf,
                      const __grid_constant__ CUtensorMap tm_pb, const double* __restrict__ sf,
-                     const double* __restrict__ pb, Dom d, WaveArgs a) {
+                     const double* __restrict__ pb, Dom d,
+                     const __grid_constant__ WaveArgs a) {
     extern __shared__ __align__(128) unsigned char smem[];
     const SlabGeom G = slab_geom(TX, d.nz);
     const int NS = a.ns;

@@ -5,6 +5,8 @@ unmodified reference by oracle/gen_golden.py), the FNV-1a-64 known answers in
 SURVEY.md section 4, the known-answer tests of test_weather.cpp, and -- when
 oracle/_ref was built -- the compiled reference itself on fresh random states.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -110,3 +112,20 @@ def test_golden_variants_agree(golden):
     # reference when the fixtures were generated
     v = golden["variants_16x16x8_s10"]
     assert v and all(x["bitwise_equal_to_reference"] for x in v.values())
+
+
+@pytest.mark.skipif(not os.path.isdir(O.CORPUS_DIR), reason="needs the reference corpus")
+@pytest.mark.parametrize("variant", [2, 3])
+@pytest.mark.parametrize("reverse", [False, True])
+def test_emitted_variants_at_default_line_length(reforacle, variant, reverse):
+    """the transpiled cpu / gpu-emulated corpus runs at the
+    default max_line_length 132 once the storage macros are expanded before the
+    line split (the reference splits first, pipeline.cpp:88 vs :103-113), bitwise
+    equal to the native reference and with its write_data cadence."""
+    g = O.make_grid()
+    s, msg = reforacle.run_variant_expand_first(variant, g, 10, 132, reverse)
+    assert s is not None, msg
+    want = reforacle.run_reference(g, 10)
+    for f, a in s.fields().items():
+        assert np.array_equal(a, want.fields()[f]), f
+    assert reforacle.last_write_calls == 1  # simple_weather.h90:93-95 at t = 0 (10 steps)

@@ -460,3 +460,41 @@ def test_concurrent_contexts_vs_oracle(coracle):
     finally:
         for ctx in ctxs:
             ctx.close()
+
+
+@pytest.mark.parametrize("calls", [[4], [2, 2], [6, 1, 2], [3, 4], [2, 1, 1, 2]])
+def test_even_calls_are_pair_passes_with_energy_u(coracle, calls):
+    """An even step count runs as pair passes only, the last one storing
+    energy_u (the intermediate field after physics) in a third buffer; odd
+    counts end with one single step.  Interleaved with uploads, downloads and
+    physics-only calls, every observable field stays bitwise the oracle's."""
+    cfg = W.GridConfig(nx=150, ny=37, nz=58, diffusion_velocity=0.14,
+                       radiation_intensity=0.21, transfer_velocity=0.03)
+    g = O.grid_from(cfg)
+    rng = np.random.default_rng(sum(calls) * 7 + len(calls))
+    n3, n2 = O.shapes(g)
+    s = O.State(rng.uniform(150, 350, n3), rng.uniform(150, 350, n3),
+                rng.uniform(150, 350, n2), rng.uniform(150, 350, n2))
+    with W.Context(cfg) as ctx:
+        assert ctx.kernel == "fused_pair"
+        for f, a in s.fields().items():
+            ctx.upload(f, np.ascontiguousarray(a))
+        for n in calls:
+            ctx.set_timing(True)
+            ctx.step(n)
+            _, singles, _ = ctx.timing(0)
+            _, pairs, _ = ctx.timing(1)
+            _, multi, _ = ctx.timing(2)
+            assert pairs == n // 2 and singles + multi == n % 2, (n, pairs, singles, multi)
+            s = coracle.steps(g, s, n)
+            assert_same({f: ctx.download(f) for f in ("energy", "energy_u", "energy_surf",
+                                                      "energy_pbl")}, s.fields(), f"{calls}/{n}")
+        # a new boundary field keeps the stored energy_u (it is not derived)
+        sf = rng.uniform(150, 350, n2)
+        ctx.upload("energy_surf", sf)
+        assert np.array_equal(ctx.download("energy_u"), s.energy_u)
+        s.energy_surf = sf
+        ctx.step(2)
+        s = coracle.steps(g, s, 2)
+        assert np.array_equal(ctx.download("energy_u"), s.energy_u)
+        assert np.array_equal(ctx.download("energy"), s.energy)
