@@ -26,6 +26,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h> // header-only NVTX v3: ranges for nsys / ncu --nvtx
+
 #include "../../include/hftw.h"
 #include "weather_kernels.cuh"
 #include "weather_pair.cuh"
@@ -37,6 +39,14 @@ using hftw::Halo;
 namespace {
 
 thread_local std::string g_err; // errors of calls without a context
+
+// NVTX range over one API call (visible in nsys timelines and ncu --nvtx filters).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 // Tuning knobs for the experiments under tools/ (HFTW_TX=32|64, HFTW_NS=stages,
 // HFTW_CHUNK=rows, ...): read ONLY in a -DHFTW_TUNING build (tools/build_variant.sh).
@@ -270,6 +280,12 @@ Halo make_halo(const hftw_ctx* c, int dst) {
         h.nsk[q] = m.sk;
         h.nb_flags[q] = m.flags;
     }
+#ifdef HFTW_TUNING
+    // timing experiments on one device (results are wrong): no pushes / no waits
+    if (env_int("HFTW_DBG_NOPUSH", 0))
+        for (int q = 0; q < hftw::kNbrs; ++q) h.nb[q] = nullptr;
+    h.nowait = env_int("HFTW_DBG_NOWAIT", 0);
+#endif
     for (int d = 0; d < 4; ++d) {
         h.slot[d] = c->plan.send_slot[d];
         h.depth[d] = c->plan.depth[d];
@@ -1521,6 +1537,7 @@ void hftw_destroy(hftw_ctx* c) {
 }
 
 int hftw_init(hftw_ctx* c) {
+    NvtxRange nvtx_("hftw_init");
     int rc = check_ctx(c);
     if (rc) return rc;
     if (is_group(c)) {
@@ -1552,6 +1569,7 @@ int hftw_init(hftw_ctx* c) {
 }
 
 int hftw_upload(hftw_ctx* c, int field, const double* host) {
+    NvtxRange nvtx_("hftw_upload");
     int rc = check_ctx(c);
     if (rc) return rc;
     if (!valid_field(field) || !host)
@@ -1585,6 +1603,7 @@ int hftw_upload(hftw_ctx* c, int field, const double* host) {
 }
 
 int hftw_download(hftw_ctx* c, int field, double* host) {
+    NvtxRange nvtx_("hftw_download");
     int rc = check_ctx(c);
     if (rc) return rc;
     if (!valid_field(field) || !host)
@@ -1615,6 +1634,7 @@ int hftw_download(hftw_ctx* c, int field, double* host) {
 }
 
 int hftw_step(hftw_ctx* c, int64_t nsteps) {
+    NvtxRange nvtx_("hftw_step");
     int rc = check_ctx(c);
     if (rc) return rc;
     if (is_group(c)) return group_step(c, nsteps);
@@ -1824,6 +1844,7 @@ int hftw_set_option(hftw_ctx* c, int opt, int64_t v) {
 }
 
 int hftw_physics(hftw_ctx* c, int mode) {
+    NvtxRange nvtx_("hftw_physics");
     int rc = check_ctx(c);
     if (rc) return rc;
     if (mode != 0 && mode != 1) return fail(c, HFTW_EINVAL, "bad physics mode %d", mode);
@@ -1839,6 +1860,7 @@ int hftw_physics(hftw_ctx* c, int mode) {
 }
 
 int hftw_diffuse(hftw_ctx* c) {
+    NvtxRange nvtx_("hftw_diffuse");
     int rc = check_ctx(c);
     if (rc) return rc;
     if (c->dist || is_group(c))
@@ -2004,6 +2026,7 @@ int hftw_peer_connect(hftw_ctx* c, const void* all, int world) {
 }
 
 int hftw_exchange(hftw_ctx* c) {
+    NvtxRange nvtx_("hftw_exchange");
     int rc = check_ctx(c);
     if (rc) return rc;
     if (is_group(c)) return group_exchange(c);
@@ -2092,6 +2115,7 @@ extern "C" {
 int hftw_simulate(hftw_ctx* c, double start_time, double end_time, double timestep,
                   double output_timestep, hftw_write_fn write, void* user, int64_t* steps_done,
                   int64_t* writes_done) {
+    NvtxRange nvtx_("hftw_simulate");
     int rc = check_ctx(c);
     if (rc) return rc;
     if (c->dist) return fail(c, HFTW_EUNSUP, "hftw_simulate runs on single-domain contexts");
@@ -2224,6 +2248,7 @@ extern "C" {
 
 int hftw_step_host(hftw_ctx* c, const double* energy, const double* energy_surf,
                    const double* energy_pbl, double* energy_out, double* energy_u_out) {
+    NvtxRange nvtx_("hftw_step_host");
     int rc = check_ctx(c);
     if (rc) return rc;
     if (!energy || !energy_surf || !energy_pbl || !energy_out || !energy_u_out)

@@ -151,6 +151,7 @@ struct Halo {
     unsigned long long* nb_flags[kNbrs]; // neighbour's flag array
     int* done;                       // CTAs of this launch that finished
     long long step;
+    int nowait;                      // HFTW_TUNING experiments only: skip the flag waits
 };
 
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
@@ -184,9 +185,17 @@ __device__ __forceinline__ void wait_flag(const unsigned long long* f, long long
 
 // Wait until every neighbour finished step-1 (mask != 0: a unit on the rim).
 __device__ __forceinline__ void halo_wait(const Halo& h, int mask) {
-    if (!h.active || !mask) return;
+    if (!h.active || !mask || h.nowait) return;
     for (int q = 0; q < kNbrs; ++q)
         if (h.nb[q]) wait_flag(&h.my_flags[q], h.step);
+}
+// The same for a thread that waits for one step many times (a producer taking
+// rim unit after rim unit): flags only grow, so once seen for `h.step` they
+// stay satisfied and the later units of that step poll nothing.
+__device__ __forceinline__ void halo_wait_once(const Halo& h, int mask, long long& seen) {
+    if (!h.active || !mask || seen == h.step) return;
+    halo_wait(h, mask);
+    seen = h.step;
 }
 
 // Store a freshly computed OWNED cell into the neighbours that need it.
@@ -209,16 +218,40 @@ __device__ __forceinline__ void halo_push(const Halo& h, const Dom& d, int i, in
     }
 }
 
-// Push the column (i, j, kl .. kl+nk-1) that this thread has just stored at src
-// (step src_sk between planes; global memory or a shared staging row) to the
-// neighbours.  Out of line: the hot loops stay small (inlined pushes cost the
-// instruction cache more than the stores), and only cells next to a face call it.
-__device__ __noinline__ void push_column(const Halo& h, const Dom& d, const double* src,
-                                         long long src_sk, int i, int j, int kl, int nk) {
-    for (int kk = 0; kk < nk; ++kk) halo_push(h, d, i, j, kl + kk, src[(long long)kk * src_sk]);
-}
-__device__ __forceinline__ bool near_face(const Dom& d, int i, int j) {
-    return i <= 2 || i >= d.nx - 1 || j <= 2 || j >= d.ny - 1;
+// Push the cells of the owned box [i0, i1] x [j0, j1] (all k) that lie within
+// two of a face, read back from u, by the `nthr` threads `tid` of a CTA -- once
+// the box's stores are complete and visible to them (a barrier).  The step
+// kernels call it per work unit on the rim, outside their row loops: pushes
+// inside the hot loops (inlined, or as a call) cost the row code 40% (register
+// pressure of the call site, instruction-cache footprint) for 0.3% of the cells.
+__device__ __forceinline__ void push_box(const Halo& h, const Dom& d, const double* u, int i0,
+                                         int i1, int j0, int j1, int tid, int nthr) {
+    int cs[4], rs[4], nc = 0, nr = 0; // the box's columns / rows next to a face
+    for (int i = i0; i <= i1 && nc < 4; ++i)
+        if (i <= 2 || i >= d.nx - 1) cs[nc++] = i;
+    for (int j = j0; j <= j1 && nr < 4; ++j)
+        if (j <= 2 || j >= d.ny - 1) rs[nr++] = j;
+    const int nj = j1 - j0 + 1, ni = i1 - i0 + 1;
+    const long long a = (long long)nc * nj;       // face columns x all rows
+    const long long b = (long long)nr * ni;       // face rows x all columns (dups skipped)
+    const long long n = (a + b) * d.nz;
+    for (long long t = tid; t < n; t += nthr) {
+        const int k = 1 + (int)(t / (a + b));
+        const long long r = t % (a + b);
+        int i, j;
+        if (r < a) {
+            i = cs[r % nc];
+            j = j0 + (int)(r / nc);
+        } else {
+            const long long q = r - a;
+            i = i0 + (int)(q % ni);
+            j = rs[q / ni];
+            bool dup = false;
+            for (int m = 0; m < nc; ++m) dup |= cs[m] == i;
+            if (dup) continue;
+        }
+        halo_push(h, d, i, j, k, u[i * d.si + j * d.sj + (long long)(k - 1) * d.sk]);
+    }
 }
 
 // A work unit (columns i0 .. i0+w-1, rows ja .. jb) reads halo slots or pushes
@@ -722,8 +755,8 @@ struct ColumnRow {
     int i, j;
 };
 
-template <bool PHYS, bool PUSH>
-__device__ __forceinline__ void column_row(const ColumnRow& r, const Halo& h, const Dom& d) {
+template <bool PHYS>
+__device__ __forceinline__ void column_row(const ColumnRow& r) {
     const int w = r.w, is = r.is, nz = r.nz;
     const double ri = r.ri, tv = r.tv, dv = r.dv, c6 = r.c6;
     auto Pc = [&](int kk) {
@@ -782,9 +815,6 @@ __device__ __forceinline__ void column_row(const ColumnRow& r, const Halo& h, co
         pd = pc;
         pc = pn;
     }
-    // decomposed: the column's cells near a face go to the neighbours (read back
-    // from where this thread just stored them)
-    if (PUSH && near_face(d, r.i, r.j)) push_column(h, d, r.up, r.sk, r.i, r.j, r.kl, r.kh - r.kl + 1);
 }
 
 template <int TX, int NCW, bool PHYS, bool KIJ>
@@ -820,6 +850,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
         // halo columns / chunk-boundary rows another CTA needs are still in L2.
         if (lane == 0) {
             uint32_t L = 0;
+            long long seen = -1; // the step whose neighbour flags this producer has seen
             for (;;) {
                 const int unit = a.u_lo + atomicAdd(&a.sched[0], 1);
                 const bool stop = unit >= a.u_hi;
@@ -834,7 +865,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
                     // to that neighbour: wait until it finished the previous step
                     const int mask = rim_unit(d, 1 + st * TX, TX, ja, jb);
                     if (h.active && mask) {
-                        halo_wait(h, mask);
+                        halo_wait_once(h, mask, seen);
                         asm volatile("fence.proxy.async.global;" ::: "memory");
                     }
                 }
@@ -921,8 +952,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
                                        (long long)(kl - 1) * d.sk;
                 const ColumnRow r{em, e0, ep, Sm, S0, Sp, Bm, B0, Bp, up, KIJ ? 1 : d.sk,
                                   w, G.is, kl, kh, nz, ri, tv, dv, c5, c6, i0 + c, j};
-                if (h.active) column_row<PHYS, true>(r, h, d);
-                else column_row<PHYS, false>(r, h, d);
+                column_row<PHYS>(r);
             }
             if (KIJ) {
                 // the row is staged: one thread stores it as ONE contiguous bulk
@@ -948,11 +978,21 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
             mbar_arrive(&empty[(lend + 1) % NS]);
         }
         L = lend + 2;
+        // decomposed rim unit: its cells near a face go to the neighbours
+        if (h.active && rim_unit(d, i0, TX, ja, jb)) {
+            if (KIJ && threadIdx.x == 0) bulk_wait_all(); // staged rows are in global memory
+            asm volatile("bar.sync 1, %0;" ::"r"(NCW * 32) : "memory");
+            push_box(h, d, u, i0, min(i0 + TX - 1, d.nx), ja, jb, threadIdx.x, NCW * 32);
+        }
     }
 
     // Epilogue: this CTA's share of the ghost cells (regions 4 and 5 of the
     // reference, 0.3% of the cells at ASUCA size), straight from global.
-    halo_wait(h, 0xF);
+    // Decomposed: after every neighbour's previous step (one poller per CTA).
+    if (h.active) {
+        if (threadIdx.x == 0) halo_wait(h, 0xF);
+        asm volatile("bar.sync 1, %0;" ::"r"(NCW * 32) : "memory");
+    }
     {
         // j-ghost rows span every owned i (the corners take the i-ghost rule
         // inside cell_update); i-ghost columns span the inner rows [r0, r1]

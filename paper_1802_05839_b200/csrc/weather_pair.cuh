@@ -310,12 +310,10 @@ __device__ __forceinline__ void inter_ghost(const IRow& r, double* out, double* 
 // neighbours and the j+1 neighbour from registers (Pc = row j, Pn = row j+1,
 // both this thread's column); only the k neighbours across the group's ends
 // come from B0.  weather.cpp:130-150 on P'.
-// hp (decomposed rim units): push the new cells near a face to the neighbours.
 template <int NK, bool FIRST, bool LAST>
 __device__ __forceinline__ void final_smem(const double* Bm, const double* B0, const double* Pc,
                                            const double* Pn, double* q, long long sk, int kl,
-                                           bool store, const Dom& d, const Halo* hp, int gi,
-                                           int j) {
+                                           bool store, const Dom& d) {
     const double dv = d.dv, c6 = d.c6, c5 = d.c5;
     const int o0 = (kl - 1) * kPairIC;
     Bm += o0;
@@ -337,14 +335,12 @@ __device__ __forceinline__ void final_smem(const double* Bm, const double* B0, c
 #pragma unroll
         for (int kk = 0; kk < NK; ++kk) q[(long long)kk * sk] = v[kk];
     }
-    if (hp) push_column(*hp, d, q, sk, gi, j, kl, NK);
 }
 
 template <int KP>
 __device__ __forceinline__ void final_smem_generic(const double* Bm, const double* B0,
                                                    const double* Bp, double* q, long long sk,
-                                                   int kl, int nk, const Dom& d, const Halo* hp,
-                                                   int gi, int j) {
+                                                   int kl, int nk, const Dom& d) {
     const int nz = d.nz;
     const double dv = d.dv;
 #pragma unroll
@@ -361,7 +357,6 @@ __device__ __forceinline__ void final_smem_generic(const double* Bm, const doubl
         else v = dadd(dmul(d.c6, B0[o]), dmul(dv, dadd(dadd(s, B0[o - kPairIC]), B0[o + kPairIC])));
         q[(long long)kk * sk] = v;
     }
-    if (hp) push_column(*hp, d, q, sk, gi, j, kl, nk);
 }
 
 // Publish the ghost-adjacent intermediates a unit owns (see PairArgs).
@@ -434,6 +429,7 @@ struct PairProducer {
     int row;   // its row (ja-2 .. jb+2)
     int jb;    // last inner row of that unit
     int slot;  // ring slot of the next load
+    bool waited; // decomposed: the neighbours' previous pass has been seen complete
 };
 
 template <bool DIST>
@@ -461,8 +457,12 @@ __device__ __forceinline__ void pair_issue(PairProducer& p, unsigned char* smem,
         p.row = ja - 2;
         if (DIST && rim_unit(d, 1 + (p.unit % a.nstrips) * kPairTX, kPairTX, ja, p.jb)) {
             // decomposed: the unit reads halo slots the neighbours filled in their
-            // previous pass and pushes into slots they read then
-            halo_wait(h, 1);
+            // previous pass and pushes into slots they read then (flags only
+            // grow: once seen, later rim units of this launch need no poll)
+            if (!p.waited) {
+                halo_wait(h, 1);
+                p.waited = true;
+            }
             asm volatile("fence.proxy.async.global;" ::: "memory");
         }
     }
@@ -519,7 +519,7 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
     const int tid = threadIdx.x;
     const int nx = d.nx, ny = d.ny, nz = d.nz;
 
-    PairProducer prod{0, 1, -2, 0}; // row > jb + 2: the first issue takes a unit
+    PairProducer prod{0, 1, -2, 0, false}; // row > jb + 2: the first issue takes a unit
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -581,9 +581,7 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
         const bool pub_row = owns_i && gi >= 1 && gi <= nx && (ja <= 2 || jb >= ny - 1);
         const int fsel = (a.fp + pair_far_col<DIST>(st, a.nstrips, d)) & 1;
         const bool do_final = cc >= 2 && cc <= kPairTX + 1 && gi <= nx && nk > 0;
-        // decomposed rim unit: final cells within two of a face go to the neighbours
-        const bool rim = DIST && rim_unit(d, i0, kPairTX, ja, jb);
-        const bool push_i = rim && (gi <= 2 || gi >= nx - 1);
+
         RingPos Ra = R0;          // slab jr-1
         RingPos Rb = Ra.next(NS); // slab jr
         RingPos Rc = Rb.next(NS); // slab jr+1
@@ -657,15 +655,12 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
                 const double* B0 = ib0 + ib1 * ibn + (cc - 1);
                 const double* Bp = ib0 + ibi * ibn + (cc - 1);
                 double* q = qrow;
-                const int j = jr - 1;
-                const Halo* hp =
-                    DIST && (push_i || (rim && (j <= 2 || j >= ny - 1))) ? &h : nullptr;
                 switch (shape) {
-                case 0: final_smem<KPT, false, false>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d, hp, gi, j); break;
-                case 4: final_smem<KPT - 1, false, false>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d, hp, gi, j); break;
-                case 5: final_smem<KPT - 1, true, false>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d, hp, gi, j); break;
-                case 6: final_smem<KPT - 1, false, true>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d, hp, gi, j); break;
-                default: final_smem_generic<KPT>(Bm, B0, Bp, q, d.sk, kl, nk, d, hp, gi, j); break;
+                case 0: final_smem<KPT, false, false>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d); break;
+                case 4: final_smem<KPT - 1, false, false>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d); break;
+                case 5: final_smem<KPT - 1, true, false>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d); break;
+                case 6: final_smem<KPT - 1, false, true>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d); break;
+                default: final_smem_generic<KPT>(Bm, B0, Bp, q, d.sk, kl, nk, d); break;
                 }
             }
             // No second barrier: the next row's target buffer (ib2) is read here only
@@ -684,6 +679,11 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
             qrow += d.sj;
         }
         R0 = Rc; // slabs jb+1, jb+2 were Ra, Rb: the next unit starts after them
+        if (DIST && rim_unit(d, i0, kPairTX, ja, jb)) {
+            // decomposed rim unit: its new cells near a face go to the neighbours
+            __syncthreads();
+            push_box(h, d, u, i0, min(i0 + kPairTX - 1, nx), ja, jb, tid, kPairThreads);
+        }
         // rim units: count the ghost producers; the second one computes the ghosts
         // (decomposed: pair_ghost_kernel, after the wrap partners published)
         const int inc_c = (st == 0) + (st == a.nstrips - 1);

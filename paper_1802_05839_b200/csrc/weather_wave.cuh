@@ -154,7 +154,6 @@ __device__ __forceinline__ void wave_consumers(unsigned char* smem, const SlabGe
     const int w = G.w, cc = c + 2;
     const double ri = d.ri, tv = d.tv, dv = d.dv, c5 = d.c5, c6 = d.c6;
     const int tid = threadIdx.x, nthreads = NCW * 32;
-    const Halo noh{};
 
     uint32_t L = 0;
     for (;;) {
@@ -218,8 +217,7 @@ __device__ __forceinline__ void wave_consumers(unsigned char* smem, const SlabGe
                              (long long)(kl - 1) * d.sk;
                 const ColumnRow row{em, e0, ep, Sm, S0, Sp, Bm, B0, Bp, up, d.sk,
                                     w, 1, kl, kh, nz, ri, tv, dv, c5, c6, i0 + c, j};
-                if (hs.active) column_row<true, true>(row, hs, d);
-                else column_row<true, false>(row, noh, d);
+                column_row<true>(row);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[l0 % NS]);
@@ -231,6 +229,11 @@ __device__ __forceinline__ void wave_consumers(unsigned char* smem, const SlabGe
             mbar_arrive(&empty[(lend + 1) % NS]);
         }
         L = lend + 2;
+        // decomposed rim unit: its cells near a face go to the neighbours
+        if (hs.active && rim_unit(d, i0, TX, ja, jb)) {
+            asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+            push_box(hs, d, u, i0, min(i0 + TX - 1, d.nx), ja, jb, tid, nthreads);
+        }
         // the i-ghost columns of these rows (their partners are in the same rows)
         const bool west = st == 0 && d.own_w, east = st == a.nstrips - 1 && d.own_e;
         if (west || east) wave_ghost_cols(e, u, sf, pb, d, hs, ja, jb, west, east, tid, nthreads);
@@ -278,6 +281,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
         // ---------------- producer: work list, dependency waits, TMA ----------------
         if (lane == 0) {
             uint32_t L = 0;
+            long long seen = -1; // the step whose neighbour flags this producer has seen
             for (;;) {
                 const int item = atomicAdd(&a.sched[0], 1);
                 const bool stop = item >= total;
@@ -322,7 +326,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
                     if (hs.active && mask) {
                         Halo hw = hs;
                         hw.step = hs.step + s;
-                        halo_wait(hw, mask);
+                        halo_wait_once(hw, mask, seen);
                     }
                     // generic-proxy writes of other CTAs -> this CTA's TMA reads
                     asm volatile("fence.proxy.async.global;" ::: "memory");
