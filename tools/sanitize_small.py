@@ -25,3 +25,16 @@ for layout in ("ijk", "kij"):
             ctx.simulate(0.0, 2.95, 0.1, 1.0, lambda tag, t, f: None)
             ctx.sync()
 print("ok")
+
+# decomposed ranks in one process (a group on this device): pair passes with the
+# ghost kernel, single steps and multi-step launches with in-kernel pushes
+for kernel, opt in (("auto", 0), ("fused_tma", 1), ("fused_tma", -1)):
+    with W.Context(W.GridConfig(nx=70, ny=45, nz=58), px=2, py=2, devices=[0] * 4,
+                   kernel=kernel) as ctx:
+        ctx.set_option("multistep", opt)
+        ctx.init()
+        ctx.step(4)
+        ctx.step(3)
+        ctx.download_state()
+        ctx.sync()
+print("ok group")
