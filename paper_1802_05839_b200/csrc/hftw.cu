@@ -125,8 +125,10 @@ struct hftw_ctx {
     size_t staging_n = 0;
     int cur = 0;               // buf[cur] holds SimState::energy
     bool eu_derived = false;   // energy_u == physics(buf[cur ^ 1]), not yet materialised
-    bool eu_stored = false;    // energy_u is in eu_buf (written by the last pair pass)
-    double* eu_buf = nullptr;  // third field buffer (allocated by the first such pass)
+    bool eu_stored = false;    // energy_u is in eu_buf (materialised after pair passes)
+    bool eu_pending = false;   // energy_u == physics(step(buf[cur ^ 1])): the call ended
+                               // with a pair pass, which keeps e_{n-1} on chip only
+    double* eu_buf = nullptr;  // third field buffer (allocated on first materialisation)
 
     // TMA kernel state
     bool tma_ok = false;
@@ -492,10 +494,8 @@ int setup_tma(hftw_ctx* c) {
 using PairKernel = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap,
                            const CUtensorMap, const double*, double*, const double*,
                            const double*, Dom, hftw::PairArgs, const Halo);
-PairKernel pair_kernel(bool dist, bool eu) {
-    using hftw::step_pair_kernel;
-    return dist ? (eu ? step_pair_kernel<kPairKPT, true, true> : step_pair_kernel<kPairKPT, true, false>)
-                : (eu ? step_pair_kernel<kPairKPT, false, true> : step_pair_kernel<kPairKPT, false, false>);
+PairKernel pair_kernel(bool dist) {
+    return dist ? hftw::step_pair_kernel<kPairKPT, true> : hftw::step_pair_kernel<kPairKPT, false>;
 }
 
 // The two-steps-per-pass kernel (weather_pair.cuh): IJK, single domain, nz
@@ -515,7 +515,7 @@ int setup_pair(hftw_ctx* c) {
     int smem_optin = 0;
     CUDA_TRY(c, cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin,
                                        c->device));
-    auto kern = pair_kernel(c->dist, true); // the largest static footprint of the four
+    auto kern = pair_kernel(c->dist);
     cudaFuncAttributes fa{};
     CUDA_TRY(c, cudaFuncGetAttributes(&fa, kern));
     const int nz = (int)c->nz;
@@ -534,8 +534,7 @@ int setup_pair(hftw_ctx* c) {
     if (!ns) return HFTW_OK;
     c->pair_ns = ns;
     c->pair_smem = hftw::pair_smem_bytes(nz, ns);
-    for (bool eu : {false, true})
-        CUDA_TRY(c, raise_smem_attr((const void*)pair_kernel(c->dist, eu), c->pair_smem));
+    CUDA_TRY(c, raise_smem_attr((const void*)kern, c->pair_smem));
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, hftw::kPairThreads,
                                                       c->pair_smem) != cudaSuccess ||
@@ -642,8 +641,7 @@ double* gpub_of(double* base, size_t per, long long pass) {
 }
 
 // Two fused steps in one launch: buf[src] -> buf[src ^ 1] = step(step(buf[src])).
-// eu: also store the intermediate field's post-physics values as energy_u.
-int launch_pair(hftw_ctx* c, int src, bool eu) {
+int launch_pair(hftw_ctx* c, int src) {
     Dom d = make_dom(c);
     hftw::PairArgs a{};
     a.fp = kFrontPad;
@@ -663,8 +661,7 @@ int launch_pair(hftw_ctx* c, int src, bool eu) {
     const Halo h = make_halo(c, src ^ 1); // pushes into the neighbours' e_{s+2}, waits >= s
     int rc = timing_mark(c, 1, true);
     if (rc) return rc;
-    if (eu) a.eu = c->eu_buf + c->off3;
-    auto kern = pair_kernel(c->dist, eu);
+    auto kern = pair_kernel(c->dist);
     kern<<<c->pair_ctas, hftw::kPairThreads, c->pair_smem, c->stream>>>(
         c->tm_e2[src], c->tm_sfpb, c->tm_ef[src], c->tm_sfpbf, e3(c, src), e3(c, src ^ 1), sf2(c),
         pb2(c), d, a, h);
@@ -712,34 +709,26 @@ int launch_pair_ghost(hftw_ctx* c, int dst) {
     return HFTW_OK;
 }
 
-// Two-step passes of an n-step call: n/2 when n is even (the last one also
-// stores energy_u, the intermediate field's post-physics values), else
-// (n-1)/2 and a final single step (energy_u = physics of the field before it
-// stays derivable from the ping-pong partner).
+// Two-step passes of an n-step call: n/2 when n is even, else (n-1)/2 and a final
+// single step.  After a pass, energy_u (physics of e_{n-1}, which the pass kept
+// on chip) is recomputed only if it is read: e_{n-2} is still in the ping-pong
+// partner (materialize_eu).
 int64_t pair_passes(int64_t nsteps) { return nsteps / 2; }
 
 // One pass: phase bit 0 launches the pair kernel, bit 1 (decomposed) the ghost
 // kernel, and then the bookkeeping.  A group on one device runs bit 0 for every
 // rank before bit 1 for any (the ghost kernels wait for the wrap partners').
-int pair_pass(hftw_ctx* c, int phase, bool eu) {
+int pair_pass(hftw_ctx* c, int phase) {
     int rc;
-    if (phase & 1) {
-        if (eu && !c->eu_buf &&
-            cudaMalloc(&c->eu_buf, c->n3 * sizeof(double)) != cudaSuccess) {
-            cudaGetLastError();
-            c->eu_buf = nullptr;
-            return fail(c, HFTW_ENOMEM, "cudaMalloc of the energy_u buffer (%zu bytes) failed",
-                        c->n3 * sizeof(double));
-        }
-        if ((rc = launch_pair(c, c->cur, eu))) return rc;
-    }
+    if ((phase & 1) && (rc = launch_pair(c, c->cur))) return rc;
     if (phase & 2) {
         if (c->dist && (rc = launch_pair_ghost(c, c->cur ^ 1))) return rc;
         c->cur ^= 1;
         c->step_count += 2;
         ++c->pass_count;
-        c->eu_stored = eu;
+        c->eu_stored = false;
         c->eu_derived = false;
+        c->eu_pending = true;
     }
     return HFTW_OK;
 }
@@ -869,10 +858,14 @@ hftw::TmaArgs tma_args(const hftw_ctx* c, const StepPart& p) {
 // Launch the fused update from buf[src] into buf[src^1]; PHYS=false is the
 // diffusion-only sweep of an already post-physics field.  `part` restricts a
 // TMA launch to a piece of the step (NULL = the whole step).
+// `out` (optional): write the step there instead of buf[src ^ 1], with no halo
+// protocol (energy_u materialisation: the halos of buf[src] are complete).
 template <bool PHYS>
-int launch_fused(hftw_ctx* c, int src, int kernel, const StepPart* part = nullptr) {
+int launch_fused(hftw_ctx* c, int src, int kernel, const StepPart* part = nullptr,
+                 double* out = nullptr) {
     Dom d = make_dom(c);
-    Halo h = make_halo(c, src ^ 1);
+    Halo h = out ? Halo{} : make_halo(c, src ^ 1);
+    double* const dst = out ? out : e3(c, src ^ 1);
     if (kernel == HFTW_KERNEL_FUSED_TMA) {
         if (!c->tma_ok) return fail(c, HFTW_EUNSUP, "TMA kernel unavailable for this grid/layout");
         const StepPart p = part ? *part : whole_step(c);
@@ -883,7 +876,7 @@ int launch_fused(hftw_ctx* c, int src, int kernel, const StepPart* part = nullpt
         dim3 block((kNCW + 1) * 32);
 #define HFTW_LAUNCH_TMA(TX, KIJ)                                                              \
     hftw::step_tma_kernel<TX, kNCW, PHYS, KIJ><<<ctas, block, c->smem, c->stream>>>(         \
-        c->tm_e[src], c->tm_sf, c->tm_pb, e3(c, src), e3(c, src ^ 1), sf2(c), pb2(c), d, a, h)
+        c->tm_e[src], c->tm_sf, c->tm_pb, e3(c, src), dst, sf2(c), pb2(c), d, a, h)
         const bool kij = c->layout == HFTW_KIJ;
         if (c->tx == 64) {
             if (kij) HFTW_LAUNCH_TMA(64, true);
@@ -900,10 +893,10 @@ int launch_fused(hftw_ctx* c, int src, int kernel, const StepPart* part = nullpt
         const int blocks = c->dist ? std::min(grid_for(c, n), c->num_sms * 4) : grid_for(c, n);
         if (c->layout == HFTW_KIJ)
             hftw::step_cell_kernel<true, PHYS><<<blocks, 256, 0, c->stream>>>(
-                e3(c, src), e3(c, src ^ 1), sf2(c), pb2(c), d, h);
+                e3(c, src), dst, sf2(c), pb2(c), d, h);
         else
             hftw::step_cell_kernel<false, PHYS><<<blocks, 256, 0, c->stream>>>(
-                e3(c, src), e3(c, src ^ 1), sf2(c), pb2(c), d, h);
+                e3(c, src), dst, sf2(c), pb2(c), d, h);
     }
     CUDA_TRY(c, cudaGetLastError());
     return HFTW_OK;
@@ -913,28 +906,28 @@ int launch_fused(hftw_ctx* c, int src, int kernel, const StepPart* part = nullpt
 // column per thread (0.366 ms at ASUCA), KIJ streamed rows (0.395 ms)
 int best_physics_mode(const hftw_ctx* c) { return c->layout == HFTW_KIJ ? 1 : 0; }
 
-int launch_physics(hftw_ctx* c, int b, int mode) {
+int launch_physics(hftw_ctx* c, double* e, int mode) {
     Dom d = make_dom(c);
     const long long cols = (c->lnx + 2) * (c->lny + 2);
     if (mode == 0) {
-        hftw::physics_column_kernel<<<grid_for(c, cols), 256, 0, c->stream>>>(e3(c, b), sf2(c),
+        hftw::physics_column_kernel<<<grid_for(c, cols), 256, 0, c->stream>>>(e, sf2(c),
                                                                              pb2(c), d);
     } else if (c->layout == HFTW_KIJ) {
         if (c->Pk >= 32 && env_int("HFTW_KIJ_PHYS_WARP", 0) == 0) { // streaming rows
             const long long tasks = (c->lny + 2) * ((c->lnx + 2 + 15) / 16);
             hftw::physics_kij_stream_kernel<<<(int)std::min<long long>((tasks + 7) / 8,
                                                                        (long long)c->num_sms * 16),
-                                              256, 0, c->stream>>>(e3(c, b), sf2(c), pb2(c), d,
+                                              256, 0, c->stream>>>(e, sf2(c), pb2(c), d,
                                                                    (int)c->Pk);
             CUDA_TRY(c, cudaGetLastError());
             return HFTW_OK;
         }
-        hftw::physics_kij_kernel<<<grid_for(c, cols * 32), 256, 0, c->stream>>>(e3(c, b), sf2(c),
+        hftw::physics_kij_kernel<<<grid_for(c, cols * 32), 256, 0, c->stream>>>(e, sf2(c),
                                                                                pb2(c), d);
     } else {
         const long long rows = (c->lny + 2) * c->nz;
         const int blocks = (int)std::min<long long>(rows, (long long)c->num_sms * 16);
-        hftw::physics_rows_kernel<<<blocks, 256, 0, c->stream>>>(e3(c, b), sf2(c), pb2(c), d);
+        hftw::physics_rows_kernel<<<blocks, 256, 0, c->stream>>>(e, sf2(c), pb2(c), d);
     }
     CUDA_TRY(c, cudaGetLastError());
     return HFTW_OK;
@@ -944,9 +937,31 @@ int launch_physics(hftw_ctx* c, int b, int mode) {
 // in the buffer that holds the previous energy (it is dead until the next step
 // overwrites it, so this is free of hazards; only owned cells are touched).
 int materialize_eu(hftw_ctx* c) {
-    if (!c->eu_derived) return HFTW_OK; // materialised, or stored by a pair pass
-    int rc = launch_physics(c, c->cur ^ 1, best_physics_mode(c));
-    if (rc) return rc;
+    int rc;
+    if (c->eu_pending) {
+        // after pair passes: energy_u = physics(e_{n-1}) and e_{n-1} = step(e_{n-2}),
+        // which the ping-pong partner still holds (with its halos): one step into the
+        // third buffer, then physics in place there
+        if (!c->eu_buf) {
+            if (cudaMalloc(&c->eu_buf, c->n3 * sizeof(double)) != cudaSuccess) {
+                cudaGetLastError();
+                c->eu_buf = nullptr;
+                return fail(c, HFTW_ENOMEM, "cudaMalloc of the energy_u buffer (%zu bytes) failed",
+                            c->n3 * sizeof(double));
+            }
+        }
+        double* out = c->eu_buf + c->off3;
+        if ((rc = launch_fused<true>(c, c->cur ^ 1,
+                                     c->tma_ok ? HFTW_KERNEL_FUSED_TMA : HFTW_KERNEL_FUSED_CELL,
+                                     nullptr, out)))
+            return rc;
+        if ((rc = launch_physics(c, out, best_physics_mode(c)))) return rc;
+        c->eu_pending = false;
+        c->eu_stored = true;
+        return HFTW_OK;
+    }
+    if (!c->eu_derived) return HFTW_OK; // materialised already
+    if ((rc = launch_physics(c, e3(c, c->cur ^ 1), best_physics_mode(c)))) return rc;
     c->eu_derived = false;
     return HFTW_OK;
 }
@@ -1300,7 +1315,7 @@ int group_step(hftw_ctx* c, int64_t nsteps) {
                 for (int phase : {1, 2})
                     for (hftw_ctx* r : c->ranks) {
                         RANK_TRY(c, r, check_ctx(r));
-                        RANK_TRY(c, r, pair_pass(r, phase, nsteps % 2 == 0 && p == pairs - 1));
+                        RANK_TRY(c, r, pair_pass(r, phase));
                     }
             nsteps -= 2 * pairs;
         }
@@ -1563,6 +1578,7 @@ int hftw_init(hftw_ctx* c) {
     CUDA_TRY(c, cudaStreamSynchronize(c->stream));
     c->eu_derived = false; // energy_u is all zeros (weather.cpp:82)
     c->eu_stored = false;
+    c->eu_pending = false;
     c->poisoned = 0;
     if (c->dist) c->halo_dirty = true;
     return HFTW_OK;
@@ -1587,6 +1603,7 @@ int hftw_upload(hftw_ctx* c, int field, const double* host) {
         rc = copy_3d(c, e3(c, c->cur ^ 1), h, true);
         c->eu_derived = false;
         c->eu_stored = false;
+        c->eu_pending = false;
         break;
     case HFTW_ENERGY_SURF:
     case HFTW_ENERGY_PBL:
@@ -1657,7 +1674,7 @@ int hftw_step(hftw_ctx* c, int64_t nsteps) {
         // derivable from the ping-pong partner
         const int64_t pairs = pair_passes(nsteps);
         for (int64_t p = 0; p < pairs; ++p)
-            if ((rc = pair_pass(c, 3, nsteps % 2 == 0 && p == pairs - 1))) return rc;
+            if ((rc = pair_pass(c, 3))) return rc;
         nsteps -= 2 * pairs;
     }
     const bool multistep = c->opt_multistep > 0 || (c->opt_multistep == 0 && c->wave_pref);
@@ -1675,6 +1692,7 @@ int hftw_step(hftw_ctx* c, int64_t nsteps) {
             c->step_count += n;
             c->eu_derived = true;
             c->eu_stored = false;
+            c->eu_pending = false;
             nsteps -= n;
         }
     }
@@ -1685,17 +1703,19 @@ int hftw_step(hftw_ctx* c, int64_t nsteps) {
         }
         if (k == HFTW_KERNEL_SPLIT) {
             // the reference's structure: physics in place, then diffusion
-            if ((rc = launch_physics(c, c->cur, best_physics_mode(c)))) return rc;
+            if ((rc = launch_physics(c, e3(c, c->cur), best_physics_mode(c)))) return rc;
             if ((rc = launch_fused<false>(c, c->cur, c->tma_ok ? HFTW_KERNEL_FUSED_TMA
                                                                : HFTW_KERNEL_FUSED_CELL)))
                 return rc;
             c->eu_derived = false;
             c->eu_stored = false;
+            c->eu_pending = false;
         } else {
             if (k1 != HFTW_KERNEL_FUSED_CELL && (rc = timing_mark(c, 0, true))) return rc;
             if ((rc = launch_fused<true>(c, c->cur, k1))) return rc;
             c->eu_derived = true;
             c->eu_stored = false;
+            c->eu_pending = false;
         }
         if ((rc = timing_mark(c, 0, false))) return rc;
         c->cur ^= 1;
@@ -1854,7 +1874,7 @@ int hftw_physics(hftw_ctx* c, int mode) {
     }
     if ((rc = check_state(c))) return rc;
     if ((rc = materialize_eu(c))) return rc;
-    if ((rc = launch_physics(c, c->cur, mode))) return rc;
+    if ((rc = launch_physics(c, e3(c, c->cur), mode))) return rc;
     if (c->dist) c->halo_dirty = true;
     return HFTW_OK;
 }
@@ -1871,6 +1891,7 @@ int hftw_diffuse(hftw_ctx* c) {
         return rc;
     c->eu_derived = false; // energy_u = the diffused input (swap semantics)
     c->eu_stored = false;
+    c->eu_pending = false;
     c->cur ^= 1;
     return HFTW_OK;
 }
@@ -2277,6 +2298,7 @@ int hftw_step_host(hftw_ctx* c, const double* energy, const double* energy_surf,
         cudaGetLastError();
         c->eu_derived = false;
         c->eu_stored = false;
+        c->eu_pending = false;
         c->poisoned = 0xF;
     }
     return rc;
@@ -2407,6 +2429,7 @@ int step_host_pipeline(hftw_ctx* c, const double* energy, const double* energy_s
     c->cur ^= 1;
     c->eu_derived = true;
     c->eu_stored = false;
+    c->eu_pending = false;
     c->poisoned = 0;
     ++c->step_count;
     return HFTW_OK;

@@ -108,8 +108,6 @@ struct PairArgs {
     int* cnt_row; // [nstrips] j-ghost producers done (chunk 0 + last chunk), self-resetting
     double* gcol; // P' at i = 0, 1, nx, nx+1: [4][ny+2][nz]
     double* grow; // P' at j = 0, 1, ny, ny+1: [4][nz][nx+2]
-    double* eu;   // EU passes: energy_u = P' (the intermediate field, post-physics) of
-                  // every owned cell, at logical (0,0,1) of a third field buffer
 };
 
 // Rows ja..jb of chunk ch.
@@ -430,6 +428,9 @@ struct PairProducer {
     int jb;    // last inner row of that unit
     int slot;  // ring slot of the next load
     bool waited; // decomposed: the neighbours' previous pass has been seen complete
+    int next;  // the next unit, claimed two slabs before the switch (-1: not yet): the
+               // scheduler atomic's latency then overlaps two rows instead of stalling
+               // warp 0 at the switch, without claiming units far ahead of their turn
 };
 
 template <bool DIST>
@@ -442,9 +443,13 @@ __device__ __forceinline__ void pair_issue(PairProducer& p, unsigned char* smem,
     if (p.unit < 0) return; // the sentinel is out: nothing left
     const int slot = p.slot;
     p.slot = slot + 1 == ns ? 0 : slot + 1;
+#ifndef HFTW_EXP_LATE_CLAIM // (A/B experiment builds only)
+    if (p.row == p.jb + 1 && p.next < 0) p.next = atomicAdd(&a.sched[0], 1);
+#endif
     if (p.row > p.jb + 2) {
         // the current unit is fully issued: take the next one
-        p.unit = atomicAdd(&a.sched[0], 1);
+        p.unit = p.next >= 0 ? p.next : atomicAdd(&a.sched[0], 1);
+        p.next = -1;
         if (p.unit >= a.nstrips * a.nchunks) {
             slot_unit[slot] = -1;
             mbar_arrive(&full[slot]); // no bytes: tells the consumers to finish
@@ -494,10 +499,7 @@ struct RingPos {
 
 // KPT: max k planes per thread (nz <= 8 * KPT).  DIST: a decomposed rank's
 // subdomain (a separate instantiation: the single-domain code is unchanged).
-// EU: the last pass of a call also stores P' as SimState::energy_u (weather.cpp:170
-// makes energy_u the post-physics field of the last step), so a call of n even
-// steps needs no trailing single steps.
-template <int KPT, bool DIST, bool EU>
+template <int KPT, bool DIST>
 __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
     step_pair_kernel(const __grid_constant__ CUtensorMap tm_e,
                      const __grid_constant__ CUtensorMap tm_sfpb,
@@ -519,7 +521,7 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
     const int tid = threadIdx.x;
     const int nx = d.nx, ny = d.ny, nz = d.nz;
 
-    PairProducer prod{0, 1, -2, 0, false}; // row > jb + 2: the first issue takes a unit
+    PairProducer prod{0, 1, -2, 0, false, -1}; // row > jb + 2: the first issue takes a unit
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -627,18 +629,11 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
                     }
                     break;
                 }
-                if (pub_col || pub_row || EU) {
+                if (pub_col || pub_row) {
                     const bool owns_j = (jr >= ja && jr <= jb) ||
                                         (DIST ? (d.own_s && jr == 0) || (d.own_n && jr == ny + 1)
                                               : jr == 0 || jr == ny + 1);
-                    if (owns_j && (pub_col || pub_row)) pair_publish<KPT>(PW2, kl, nk, gi, jr, d, a);
-                    if (EU && owns_j && owns_i) {
-                        double* q = a.eu + (long long)gi * d.si + (long long)jr * d.sj +
-                                    (long long)(kl - 1) * d.sk;
-#pragma unroll
-                        for (int kk = 0; kk < KPT; ++kk)
-                            if (kk < nk) q[(long long)kk * d.sk] = PW2[kk];
-                    }
+                    if (owns_j) pair_publish<KPT>(PW2, kl, nk, gi, jr, d, a);
                 }
             }
             __syncthreads(); // intermediate row jr complete; slab jr-1 free

@@ -464,10 +464,11 @@ def test_concurrent_contexts_vs_oracle(coracle):
 
 @pytest.mark.parametrize("calls", [[4], [2, 2], [6, 1, 2], [3, 4], [2, 1, 1, 2]])
 def test_even_calls_are_pair_passes_with_energy_u(coracle, calls):
-    """An even step count runs as pair passes only, the last one storing
-    energy_u (the intermediate field after physics) in a third buffer; odd
-    counts end with one single step.  Interleaved with uploads, downloads and
-    physics-only calls, every observable field stays bitwise the oracle's."""
+    """An even step count runs as pair passes only (energy_u, the physics of the
+    step before the last, is recomputed from the ping-pong partner when it is
+    read); odd counts end with one single step.  Interleaved with uploads,
+    downloads and boundary-field changes, every observable field stays bitwise
+    the oracle's."""
     cfg = W.GridConfig(nx=150, ny=37, nz=58, diffusion_velocity=0.14,
                        radiation_intensity=0.21, transfer_velocity=0.03)
     g = O.grid_from(cfg)
@@ -489,7 +490,10 @@ def test_even_calls_are_pair_passes_with_energy_u(coracle, calls):
             s = coracle.steps(g, s, n)
             assert_same({f: ctx.download(f) for f in ("energy", "energy_u", "energy_surf",
                                                       "energy_pbl")}, s.fields(), f"{calls}/{n}")
-        # a new boundary field keeps the stored energy_u (it is not derived)
+        # the boundary field changes while energy_u is still pending (not read since
+        # the pass): it keeps the values of the steps that produced it
+        ctx.step(2)
+        s = coracle.steps(g, s, 2)
         sf = rng.uniform(150, 350, n2)
         ctx.upload("energy_surf", sf)
         assert np.array_equal(ctx.download("energy_u"), s.energy_u)
