@@ -428,9 +428,6 @@ struct PairProducer {
     int jb;    // last inner row of that unit
     int slot;  // ring slot of the next load
     bool waited; // decomposed: the neighbours' previous pass has been seen complete
-    int next;  // the next unit, claimed two slabs before the switch (-1: not yet): the
-               // scheduler atomic's latency then overlaps two rows instead of stalling
-               // warp 0 at the switch, without claiming units far ahead of their turn
 };
 
 template <bool DIST>
@@ -443,13 +440,9 @@ __device__ __forceinline__ void pair_issue(PairProducer& p, unsigned char* smem,
     if (p.unit < 0) return; // the sentinel is out: nothing left
     const int slot = p.slot;
     p.slot = slot + 1 == ns ? 0 : slot + 1;
-#ifndef HFTW_EXP_LATE_CLAIM // (A/B experiment builds only)
-    if (p.row == p.jb + 1 && p.next < 0) p.next = atomicAdd(&a.sched[0], 1);
-#endif
     if (p.row > p.jb + 2) {
         // the current unit is fully issued: take the next one
-        p.unit = p.next >= 0 ? p.next : atomicAdd(&a.sched[0], 1);
-        p.next = -1;
+        p.unit = atomicAdd(&a.sched[0], 1);
         if (p.unit >= a.nstrips * a.nchunks) {
             slot_unit[slot] = -1;
             mbar_arrive(&full[slot]); // no bytes: tells the consumers to finish
@@ -521,7 +514,7 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
     const int tid = threadIdx.x;
     const int nx = d.nx, ny = d.ny, nz = d.nz;
 
-    PairProducer prod{0, 1, -2, 0, false, -1}; // row > jb + 2: the first issue takes a unit
+    PairProducer prod{0, 1, -2, 0, false}; // row > jb + 2: the first issue takes a unit
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
