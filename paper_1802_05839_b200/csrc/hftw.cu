@@ -702,8 +702,10 @@ int launch_pair_ghost(hftw_ctx* c, int dst) {
     g.grow_n = part[HFTW_N];
     g.pub = c->step_count + 2;
     const long long cells = 2 * (c->lny + 2 + c->lnx) * c->nz;
+    // few CTAs: each polls the wrap partners' flags (system-scope acquires) once
     const int blocks = (int)std::max<long long>(
-        1, std::min<long long>((cells + 255) / 256, (long long)c->num_sms * 2));
+        1, std::min<long long>((cells + 1023) / 1024,
+                               (long long)env_int("HFTW_GHOST_CTAS", c->num_sms / 2)));
     hftw::pair_ghost_kernel<<<blocks, 256, 0, c->stream>>>(e3(c, dst), d, h, g);
     CUDA_TRY(c, cudaGetLastError());
     return HFTW_OK;

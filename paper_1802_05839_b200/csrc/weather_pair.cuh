@@ -741,7 +741,7 @@ struct PairGhostArgs {
 __global__ void __launch_bounds__(256) pair_ghost_kernel(double* __restrict__ u, Dom d, Halo h,
                                                          PairGhostArgs g) {
     const int nx = d.nx, ny = d.ny, nz = d.nz;
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && !h.nowait) {
         for (int q = 0; q < 4; ++q)
             if (g.wait[q]) wait_flag(&h.my_flags[kPubFlag + q], g.pub);
     }
@@ -764,10 +764,12 @@ __global__ void __launch_bounds__(256) pair_ghost_kernel(double* __restrict__ u,
         int i, j, k;
         double v;
         if (t < nw + ne) {
+            // k fastest: the published columns are [w][j][k], so a warp reads 32
+            // consecutive values of each
             const bool west = t < nw;
             const long long q = west ? t : t - nw;
-            j = o.j0 + (int)(q % nr);
-            k = 1 + (int)(q / nr);
+            k = 1 + (int)(q % nz);
+            j = o.j0 + (int)(q / nz);
             if (west) { // (1-2dv) P'(0) + dv (P'(1) + P'(gnx))
                 i = 0;
                 v = dadd(dmul(d.c2, C(g.gcol, 0, j, k)),
