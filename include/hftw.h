@@ -162,7 +162,11 @@ int hftw_get_kernel(const hftw_ctx* ctx);
 enum hftw_option {
     HFTW_OPT_MULTISTEP = 1, /* single-step kernel, n >= 2 steps in ONE persistent launch:
                                -1 never, 0 where a step is short (default), 1 always */
-    HFTW_OPT_PAIR = 2       /* AUTO may use two-step passes: 1 (default) or 0 */
+    HFTW_OPT_PAIR = 2,      /* AUTO may use two-step passes: 1 (default) or 0 */
+    HFTW_OPT_EXCHANGE = 3   /* group contexts: 0 the step kernels push the halos (default);
+                               1 the un-overlapped baseline -- steps without the halo
+                               protocol, then a separate face-copy kernel per rank and
+                               event waits (single-step kernels only; measurement) */
 };
 int hftw_set_option(hftw_ctx* ctx, int option, int64_t value);
 

@@ -166,6 +166,8 @@ struct hftw_ctx {
     int wave_chunk = 0, wave_nchunks = 0, wave_ctas = 0, wave_gtasks = 0;
     bool wave_pref = false;     // multi-step launch preferred over one launch per step (auto)
     int opt_multistep = 0;      // HFTW_OPT_MULTISTEP: -1 never, 0 auto (wave_pref), 1 always
+    int opt_exchange = 0;       // HFTW_OPT_EXCHANGE (groups): 0 in-kernel pushes, 1 baseline
+    cudaEvent_t xev = nullptr;  // the baseline's "my faces are out" event
     int* d_wave = nullptr;      // sched[2] + chunk_done[nchunks] + ghost_done[1]
 
     // measurement hook (hftw_set_timing)
@@ -576,18 +578,14 @@ int setup_pair(hftw_ctx* c) {
     long long chunk = env_int("HFTW_PAIR_CHUNK", 0);
     const long long slots = (long long)per_sm * c->num_sms;
     if (chunk <= 0) {
-        double best = 1e30;
-        // (measured at ASUCA size: 16-row units beat longer ones, whose tail
-        // at the end of the launch costs more than their halo rows save)
-        for (long long ch = std::min<long long>(16, ny); ch >= 1; --ch) {
-            const long long units = (long long)c->pair_nstrips * ((ny + ch - 1) / ch);
-            const double waves = (double)((units + slots - 1) / slots);
-            const double cost = waves * (double)(ch + 4);
-            if (cost < best - 1e-9) {
-                best = cost;
-                chunk = ch;
-            }
-        }
+        // Rows per unit by how many waves of 16-row units a pass has (measured with
+        // tools/group_diag.py and HFTW_PAIR_CHUNK, profiles/r02_chunk_sweep.txt):
+        // >= 5 waves 16 rows (ASUCA, 14.7 waves: 0.519 ms per pass vs 0.534 at 12 and
+        // 0.554 at 8 -- longer units also lose, to the launch tail), 2.5-5 waves 12
+        // (a 2x2 rank: 0.187 vs 0.192 at 16), fewer 8 (a 2x4 rank: 0.122 vs 0.133):
+        // short passes need more units to fill both CTAs of every SM.
+        const double w16 = (double)((long long)c->pair_nstrips * ((ny + 15) / 16)) / (double)slots;
+        chunk = w16 >= 5.0 ? 16 : w16 >= 2.5 ? 12 : 8;
     }
     c->pair_chunk = (int)std::min<long long>(chunk, ny);
     // the last ~1.5 waves of units get half-height chunks (a shorter tail)
@@ -864,9 +862,9 @@ hftw::TmaArgs tma_args(const hftw_ctx* c, const StepPart& p) {
 // protocol (energy_u materialisation: the halos of buf[src] are complete).
 template <bool PHYS>
 int launch_fused(hftw_ctx* c, int src, int kernel, const StepPart* part = nullptr,
-                 double* out = nullptr) {
+                 double* out = nullptr, bool no_halo = false) {
     Dom d = make_dom(c);
-    Halo h = out ? Halo{} : make_halo(c, src ^ 1);
+    Halo h = out || no_halo ? Halo{} : make_halo(c, src ^ 1);
     double* const dst = out ? out : e3(c, src ^ 1);
     if (kernel == HFTW_KERNEL_FUSED_TMA) {
         if (!c->tma_ok) return fail(c, HFTW_EUNSUP, "TMA kernel unavailable for this grid/layout");
@@ -1307,6 +1305,55 @@ int group_step(hftw_ctx* c, int64_t nsteps) {
             if (rc) return rc;
             break;
         }
+    if (c->ranks[0]->opt_exchange == 1) {
+        // the un-overlapped baseline: every rank's step without the halo
+        // protocol, then its faces copied into the neighbours by a separate
+        // kernel; the next step of a rank waits for its neighbours' copies
+        const int k = resolved_kernel(c->ranks[0]);
+        if (k != HFTW_KERNEL_FUSED_TMA && k != HFTW_KERNEL_FUSED_CELL)
+            return fail(c, HFTW_EUNSUP, "HFTW_OPT_EXCHANGE = 1 takes a single-step kernel "
+                                        "(hftw_set_kernel fused_tma or fused_cell)");
+        for (hftw_ctx* r : c->ranks) RANK_TRY(c, r, hftw_sync(r)); // earlier pushes landed
+        for (hftw_ctx* r : c->ranks)
+            if (!r->xev) {
+                RANK_TRY(c, r, check_ctx(r));
+                if (cudaEventCreateWithFlags(&r->xev, cudaEventDisableTiming) != cudaSuccess)
+                    return fail(c, HFTW_ECUDA, "event creation failed");
+            }
+        for (int64_t s = 0; s < nsteps; ++s) {
+            for (hftw_ctx* r : c->ranks) {
+                RANK_TRY(c, r, check_ctx(r));
+                if (s > 0)
+                    for (int q = 0; q < hftw::kNbrs; ++q) {
+                        const int nr = nbr_rank(r->plan, q);
+                        if (nr >= 0)
+                            CUDA_TRY(c, cudaStreamWaitEvent(r->stream, c->ranks[(size_t)nr]->xev, 0));
+                    }
+                RANK_TRY(c, r, launch_fused<true>(r, r->cur, k, nullptr, nullptr, true));
+            }
+            for (hftw_ctx* r : c->ranks) {
+                RANK_TRY(c, r, check_ctx(r));
+                const int dst = r->cur ^ 1;
+                const Halo h = make_halo(r, dst);
+                const Box o = owned_box(r);
+                const long long cells = 4 * (o.i1 - o.i0 + o.j1 - o.j0 + 2) * r->nz;
+                hftw::face_push_kernel<<<grid_for(r, cells), 256, 0, r->stream>>>(
+                    e3(r, dst), make_dom(r), h);
+                CUDA_TRY(c, cudaGetLastError());
+                CUDA_TRY(c, cudaEventRecord(r->xev, r->stream));
+            }
+            for (hftw_ctx* r : c->ranks) {
+                r->cur ^= 1;
+                ++r->step_count;
+                r->eu_derived = true;
+                r->eu_stored = false;
+                r->eu_pending = false;
+            }
+        }
+        // the next call's first steps may use the flag protocol again: every rank
+        // waits for every copy, and the step flags restart from here
+        return group_exchange(c);
+    }
     if (c->interleave) {
         // ranks sharing a device: every launch of a pass for all ranks, in rank
         // order, before any launch that waits for it
@@ -1543,6 +1590,7 @@ void hftw_destroy(hftw_ctx* c) {
         if (o.host) cudaFreeHost(o.host);
     }
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    if (c->xev) cudaEventDestroy(c->xev);
     if (c->h2d_stream) cudaStreamDestroy(c->h2d_stream);
     if (c->d2h_stream) cudaStreamDestroy(c->d2h_stream);
     for (cudaEvent_t e : c->pipe_ev) cudaEventDestroy(e);
@@ -1860,6 +1908,10 @@ int hftw_set_option(hftw_ctx* c, int opt, int64_t v) {
     case HFTW_OPT_PAIR:
         if (v != 0 && v != 1) return fail(c, HFTW_EINVAL, "HFTW_OPT_PAIR takes 0 or 1");
         c->pair_auto = v != 0;
+        return HFTW_OK;
+    case HFTW_OPT_EXCHANGE:
+        if (v != 0 && v != 1) return fail(c, HFTW_EINVAL, "HFTW_OPT_EXCHANGE takes 0 or 1");
+        c->opt_exchange = (int)v;
         return HFTW_OK;
     }
     return fail(c, HFTW_EINVAL, "unknown option %d", opt);

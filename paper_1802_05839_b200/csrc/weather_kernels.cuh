@@ -162,6 +162,13 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// After ONE system-scope fence (__threadfence_system), relaxed stores of several
+// flags are each a release (the PTX fence-then-relaxed-store pattern): a release
+// store per flag would repeat the system-wide fence for every neighbour -- 8 of
+// them cost a decomposed pass's ghost kernel ~15 us.
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 
 // Spin-wait watchdog: a flag wait that cannot end (a neighbour rank died or
 // was never launched) traps after kSpinLimitNs, so the launch fails with an
@@ -268,7 +275,7 @@ __device__ __forceinline__ void halo_signal(const Halo& h) {
     if (atomicAdd(h.done, 1) == (int)gridDim.x - 1) {
         __threadfence_system();
         for (int q = 0; q < kNbrs; ++q)
-            if (h.nb[q]) st_release_sys(&h.nb_flags[q][opp_dir(q)], (unsigned long long)(h.step + 1));
+            if (h.nb[q]) st_relaxed_sys(&h.nb_flags[q][opp_dir(q)], (unsigned long long)(h.step + 1));
         *h.done = 0;
         __threadfence();
     }
@@ -320,6 +327,15 @@ __global__ void __launch_bounds__(256) step_cell_kernel(const double* __restrict
         __syncthreads();
         if (threadIdx.x == 0) halo_signal(h);
     }
+}
+
+// The un-overlapped exchange baseline (HFTW_OPT_EXCHANGE = 1): after a step
+// without pushes, copy this rank's cells near the faces into the neighbours.
+__global__ void __launch_bounds__(256) face_push_kernel(const double* __restrict__ u, Dom d,
+                                                        const __grid_constant__ Halo h) {
+    const Owned o = owned(d);
+    push_box(h, d, u, o.i0, o.i1, o.j0, o.j1, blockIdx.x * blockDim.x + threadIdx.x,
+             gridDim.x * blockDim.x);
 }
 
 // Initial / post-upload halo fill: push the current field's owned cells and

@@ -711,7 +711,7 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
                 __threadfence_system();
                 for (int q = 0; q < 4; ++q)
                     if (h.nb[q] && h.depth[q] == 1)
-                        st_release_sys(&h.nb_flags[q][kPubFlag + opp_dir(q)],
+                        st_relaxed_sys(&h.nb_flags[q][kPubFlag + opp_dir(q)],
                                        (unsigned long long)(h.step + 2));
             }
             __threadfence();

@@ -131,7 +131,7 @@ __device__ __forceinline__ void wave_item_done(const WaveArgs& a, int s, int per
     if (atomicAdd(&a.step_done[s], 1) == per_step - 1) {
         __threadfence_system();
         for (int q = 0; q < kNbrs; ++q)
-            if (h.nb[q]) st_release_sys(&h.nb_flags[q][opp_dir(q)], (unsigned long long)(h.step + s + 1));
+            if (h.nb[q]) st_relaxed_sys(&h.nb_flags[q][opp_dir(q)], (unsigned long long)(h.step + s + 1));
     }
 }
 

@@ -167,3 +167,22 @@ def test_asuca_default_path_vs_reference_hash(golden, coracle):
             assert pairs >= (steps - 2) // 2
             for f, v in h["fnv1a64"].items():
                 assert coracle.fnv(ctx.download(f)) == v, (steps, f)
+
+
+@pytest.mark.parametrize("grid", [(2, 1), (2, 2), (2, 4)])
+def test_exchange_baseline_bitwise(coracle, grid):
+    """HFTW_OPT_EXCHANGE = 1 (the un-overlapped baseline: steps without the halo
+    protocol, a separate face-copy kernel per rank) gives the same bits, and the
+    flag protocol resumes after it."""
+    cfg = W.GridConfig(nx=131, ny=97, nz=12, diffusion_velocity=0.125)
+    s0 = random_state(cfg, 3)
+    want = coracle.steps(O.grid_from(cfg), s0, 5).fields()
+    with group(cfg, *grid, kernel="fused_tma") as ctx:
+        for f, a in s0.fields().items():
+            ctx.upload(f, np.ascontiguousarray(a))
+        ctx.set_option("exchange", 1)
+        ctx.step(3)
+        ctx.set_option("exchange", 0)
+        ctx.step(2)
+        got = {f: ctx.download(f) for f in FIELDS}
+    assert_bitwise(got, want, f"baseline {grid}")
