@@ -233,10 +233,12 @@ __device__ __forceinline__ void halo_push(const Halo& h, const Dom& d, int i, in
 // pressure of the call site, instruction-cache footprint) for 0.3% of the cells.
 __device__ __forceinline__ void push_box(const Halo& h, const Dom& d, const double* u, int i0,
                                          int i1, int j0, int j1, int tid, int nthr) {
-    int cs[4], rs[4], nc = 0, nr = 0; // the box's columns / rows next to a face
-    for (int i = i0; i <= i1 && nc < 4; ++i)
+    // the box's columns / rows next to a face: 0..2 and n-1..n+1, up to six when
+    // the box spans both faces (a whole owned box, or a narrow subdomain)
+    int cs[6], rs[6], nc = 0, nr = 0;
+    for (int i = i0; i <= i1 && nc < 6; ++i)
         if (i <= 2 || i >= d.nx - 1) cs[nc++] = i;
-    for (int j = j0; j <= j1 && nr < 4; ++j)
+    for (int j = j0; j <= j1 && nr < 6; ++j)
         if (j <= 2 || j >= d.ny - 1) rs[nr++] = j;
     const int nj = j1 - j0 + 1, ni = i1 - i0 + 1;
     const long long a = (long long)nc * nj;       // face columns x all rows
