@@ -41,9 +41,9 @@ METRIC = "grid-cell updates/sec per timestep and achieved HBM GB/s vs peak"
 UNIT = "cell-updates/s"
 WORKLOADS = {
     # name: (grid, short description; the driver truncates long strings)
-    "full": ((1581, 1301, 58), "full timestep (physics + diffusion), ASUCA 1581x1301x58 fp64"),
-    "stencil": ((256, 256, 64), "diffusion stencil only, 256x256x64 fp64"),
-    "physics": ((1581, 1301, 58), "column physics only, ASUCA 1581x1301x58 fp64"),
+    "full": ((1581, 1301, 58), "full step 1581x1301x58 f64"),
+    "stencil": ((256, 256, 64), "stencil only 256x256x64 f64"),
+    "physics": ((1581, 1301, 58), "physics only 1581x1301x58 f64"),
 }
 
 

@@ -126,6 +126,7 @@ struct hftw_ctx {
     int cur = 0;               // buf[cur] holds SimState::energy
     bool eu_derived = false;   // energy_u == physics(buf[cur ^ 1]), not yet materialised
     bool eu_stored = false;    // energy_u is in eu_buf (materialised after pair passes)
+    bool partner_pform = false; // with eu_pending: buf[cur ^ 1] holds P(e_{n-2}), not e_{n-2}
     bool eu_pending = false;   // energy_u == physics(step(buf[cur ^ 1])): the call ended
                                // with a pair pass, which keeps e_{n-1} on chip only
     double* eu_buf = nullptr;  // third field buffer (allocated on first materialisation)
@@ -496,8 +497,18 @@ int setup_tma(hftw_ctx* c) {
 using PairKernel = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap,
                            const CUtensorMap, const double*, double*, const double*,
                            const double*, Dom, hftw::PairArgs, const Halo);
-PairKernel pair_kernel(bool dist) {
-    return dist ? hftw::step_pair_kernel<kPairKPT, true> : hftw::step_pair_kernel<kPairKPT, false>;
+// form (single domain): kPairIn = e_s is stored post-physics, kPairOut = store
+// e_{s+2} post-physics (the passes of one call between its first and last)
+constexpr int kPairIn = 1, kPairOut = 2;
+PairKernel pair_kernel(bool dist, int form = 0) {
+    using namespace hftw;
+    if (dist) return step_pair_kernel<kPairKPT, true, false, false>;
+    switch (form) {
+    case kPairIn: return step_pair_kernel<kPairKPT, false, true, false>;
+    case kPairOut: return step_pair_kernel<kPairKPT, false, false, true>;
+    case kPairIn | kPairOut: return step_pair_kernel<kPairKPT, false, true, true>;
+    default: return step_pair_kernel<kPairKPT, false, false, false>;
+    }
 }
 
 // The two-steps-per-pass kernel (weather_pair.cuh): IJK, single domain, nz
@@ -536,7 +547,8 @@ int setup_pair(hftw_ctx* c) {
     if (!ns) return HFTW_OK;
     c->pair_ns = ns;
     c->pair_smem = hftw::pair_smem_bytes(nz, ns);
-    CUDA_TRY(c, raise_smem_attr((const void*)kern, c->pair_smem));
+    for (int form = 0; form < (c->dist ? 1 : 4); ++form)
+        CUDA_TRY(c, raise_smem_attr((const void*)pair_kernel(c->dist, form), c->pair_smem));
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, hftw::kPairThreads,
                                                       c->pair_smem) != cudaSuccess ||
@@ -638,8 +650,9 @@ double* gpub_of(double* base, size_t per, long long pass) {
     return base + (size_t)(pass & 1) * per;
 }
 
-// Two fused steps in one launch: buf[src] -> buf[src ^ 1] = step(step(buf[src])).
-int launch_pair(hftw_ctx* c, int src) {
+// Two fused steps in one launch: buf[src] -> buf[src ^ 1] = step(step(buf[src])),
+// either side stored post-physics as `form` says (pair_kernel).
+int launch_pair(hftw_ctx* c, int src, int form) {
     Dom d = make_dom(c);
     hftw::PairArgs a{};
     a.fp = kFrontPad;
@@ -659,7 +672,7 @@ int launch_pair(hftw_ctx* c, int src) {
     const Halo h = make_halo(c, src ^ 1); // pushes into the neighbours' e_{s+2}, waits >= s
     int rc = timing_mark(c, 1, true);
     if (rc) return rc;
-    auto kern = pair_kernel(c->dist);
+    auto kern = pair_kernel(c->dist, c->dist ? 0 : form);
     kern<<<c->pair_ctas, hftw::kPairThreads, c->pair_smem, c->stream>>>(
         c->tm_e2[src], c->tm_sfpb, c->tm_ef[src], c->tm_sfpbf, e3(c, src), e3(c, src ^ 1), sf2(c),
         pb2(c), d, a, h);
@@ -718,9 +731,9 @@ int64_t pair_passes(int64_t nsteps) { return nsteps / 2; }
 // One pass: phase bit 0 launches the pair kernel, bit 1 (decomposed) the ghost
 // kernel, and then the bookkeeping.  A group on one device runs bit 0 for every
 // rank before bit 1 for any (the ghost kernels wait for the wrap partners').
-int pair_pass(hftw_ctx* c, int phase) {
+int pair_pass(hftw_ctx* c, int phase, int form = 0) {
     int rc;
-    if ((phase & 1) && (rc = launch_pair(c, c->cur))) return rc;
+    if ((phase & 1) && (rc = launch_pair(c, c->cur, form))) return rc;
     if (phase & 2) {
         if (c->dist && (rc = launch_pair_ghost(c, c->cur ^ 1))) return rc;
         c->cur ^= 1;
@@ -729,6 +742,7 @@ int pair_pass(hftw_ctx* c, int phase) {
         c->eu_stored = false;
         c->eu_derived = false;
         c->eu_pending = true;
+        c->partner_pform = (form & kPairIn) != 0; // the pass's input is now the partner
     }
     return HFTW_OK;
 }
@@ -951,9 +965,11 @@ int materialize_eu(hftw_ctx* c) {
             }
         }
         double* out = c->eu_buf + c->off3;
-        if ((rc = launch_fused<true>(c, c->cur ^ 1,
-                                     c->tma_ok ? HFTW_KERNEL_FUSED_TMA : HFTW_KERNEL_FUSED_CELL,
-                                     nullptr, out)))
+        const int k1 = c->tma_ok ? HFTW_KERNEL_FUSED_TMA : HFTW_KERNEL_FUSED_CELL;
+        // the partner holds P(e_{n-2}) when the last pass read a post-physics field:
+        // then the step is the diffusion sweep alone
+        if ((rc = c->partner_pform ? launch_fused<false>(c, c->cur ^ 1, k1, nullptr, out)
+                                   : launch_fused<true>(c, c->cur ^ 1, k1, nullptr, out)))
             return rc;
         if ((rc = launch_physics(c, out, best_physics_mode(c)))) return rc;
         c->eu_pending = false;
@@ -1722,9 +1738,13 @@ int hftw_step(hftw_ctx* c, int64_t nsteps) {
         // pairs, then one or two single steps: the last step is a single-step
         // launch so that energy_u (physics of the field before it) stays
         // derivable from the ping-pong partner
+        // single domain: between the passes of this call the field is stored
+        // post-physics (the first pass reads, the last one writes, plain e)
         const int64_t pairs = pair_passes(nsteps);
-        for (int64_t p = 0; p < pairs; ++p)
-            if ((rc = pair_pass(c, 3))) return rc;
+        for (int64_t p = 0; p < pairs; ++p) {
+            const int form = c->dist ? 0 : (p > 0 ? kPairIn : 0) | (p + 1 < pairs ? kPairOut : 0);
+            if ((rc = pair_pass(c, 3, form))) return rc;
+        }
         nsteps -= 2 * pairs;
     }
     const bool multistep = c->opt_multistep > 0 || (c->opt_multistep == 0 && c->wave_pref);

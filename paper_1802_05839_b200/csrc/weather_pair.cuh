@@ -157,7 +157,9 @@ struct IRow {
 // last plane is nz (:146-149, pb correction :126-127); every other plane is
 // the inner stencil (:130-137) with P = e + ri.  All branches are resolved at
 // compile time and every offset is a constant.
-template <int KP, int NK, bool FIRST, bool LAST>
+// PIN: the slabs already hold post-physics values (the previous pass stored
+// them, POUT), so the loads are used as they are.
+template <int KP, int NK, bool FIRST, bool LAST, bool PIN>
 __device__ __forceinline__ void inter_inner(const IRow& r, double* out, double* ib, int kl,
                                             const Dom& d) {
     constexpr int W = kPairW;
@@ -167,35 +169,34 @@ __device__ __forceinline__ void inter_inner(const IRow& r, double* out, double* 
     const double* pp = r.ep + (kl - 1) * W;
     double* q = ib + (kl - 1) * kPairIC; // ib: this row's buffer, never null here
     auto corr = [&](double x, double bnd) { return dsub(x, dmul(tv, dsub(x, bnd))); };
+    // post-physics value of a loaded element: inner plane / plane 1 or nz
+    auto Pi = [&](double x) { return PIN ? x : dadd(x, ri); };
+    auto Pb = [&](double x, double bnd) { return PIN ? x : corr(dadd(x, ri), bnd); };
     const double* sfr = r.S0;     // sf row (pb is W further)
     // window: pd = P(k-1), pc = P(k).  The fast shapes are used only when every
     // group has >= 2 planes (nz >= 16), so the planes next to a group (kl-1,
     // kh+1) are never 1 or nz unless the group itself is FIRST / LAST.
-    double pd = FIRST ? 0.0 : dadd(p0[-W], ri);
-    double pc = FIRST ? corr(dadd(p0[0], ri), sfr[0]) : dadd(p0[0], ri);
+    double pd = FIRST ? 0.0 : Pi(p0[-W]);
+    double pc = FIRST ? Pb(p0[0], sfr[0]) : Pi(p0[0]);
 #pragma unroll
     for (int kk = 0; kk < NK; ++kk) {
         const int o = kk * W;
         const bool top = FIRST && kk == 0;       // plane 1
         const bool bot = LAST && kk == NK - 1;   // plane nz
         double pn = 0.0;
-        if (!bot) {
-            pn = dadd(p0[o + W], ri);
-            if (LAST && kk == NK - 2) pn = corr(pn, sfr[W]); // plane nz
-        }
+        if (!bot) pn = LAST && kk == NK - 2 ? Pb(p0[o + W], sfr[W]) : Pi(p0[o + W]); // nz
         double v;
         if (top || bot) {
             const int bo = top ? 0 : W;
-            double s = dadd(corr(dadd(p0[o - 1], ri), sfr[bo - 1]),
-                            corr(dadd(p0[o + 1], ri), sfr[bo + 1]));
-            s = dadd(s, corr(dadd(pm[o], ri), r.Sm[bo]));
-            s = dadd(s, corr(dadd(pp[o], ri), r.Sp[bo]));
+            double s = dadd(Pb(p0[o - 1], sfr[bo - 1]), Pb(p0[o + 1], sfr[bo + 1]));
+            s = dadd(s, Pb(pm[o], r.Sm[bo]));
+            s = dadd(s, Pb(pp[o], r.Sp[bo]));
             const double u = dadd(dmul(c5, pc), dmul(dv, dadd(s, top ? pn : pd)));
             v = corr(dadd(u, ri), sfr[bo]);
         } else {
-            double s = dadd(dadd(p0[o - 1], ri), dadd(p0[o + 1], ri));
-            s = dadd(s, dadd(pm[o], ri));
-            s = dadd(s, dadd(pp[o], ri));
+            double s = dadd(Pi(p0[o - 1]), Pi(p0[o + 1]));
+            s = dadd(s, Pi(pm[o]));
+            s = dadd(s, Pi(pp[o]));
             const double u = dadd(dmul(c6, pc), dmul(dv, dadd(dadd(s, pd), pn)));
             v = dadd(u, ri);
         }
@@ -212,14 +213,17 @@ __device__ __forceinline__ void inter_inner(const IRow& r, double* out, double* 
 
 // Generic (any plane range, runtime nk <= KP): Pfull everywhere.  Used only
 // for grids whose k-groups match no compile-time shape (small or odd nz).
-template <int KP>
+template <int KP, bool PIN>
 __device__ __forceinline__ void inter_generic(const IRow& r, double* out, double* ib, int kl,
                                               int nk, const Dom& d) {
     constexpr int W = kPairW;
     const int nz = d.nz;
     const double ri = d.ri, tv = d.tv, dv = d.dv;
     const double* B0 = r.S0 + W;
-    auto Pc = [&](int k) { return Pfull(r.e0[(k - 1) * W], k, nz, r.S0[0], B0[0], ri, tv); };
+    auto Pl = [&](double x, int k, double sfv, double pbv) {
+        return PIN ? x : Pfull(x, k, nz, sfv, pbv, ri, tv);
+    };
+    auto Pc = [&](int k) { return Pl(r.e0[(k - 1) * W], k, r.S0[0], B0[0]); };
     double pd = kl > 1 ? Pc(kl - 1) : 0.0;
     double pc = Pc(kl);
 #pragma unroll
@@ -228,10 +232,9 @@ __device__ __forceinline__ void inter_generic(const IRow& r, double* out, double
         const int k = kl + kk;
         const int o = (k - 1) * W;
         const double pn = k < nz ? Pc(k + 1) : 0.0;
-        double s = dadd(Pfull(r.e0[o - 1], k, nz, r.S0[-1], B0[-1], ri, tv),
-                        Pfull(r.e0[o + 1], k, nz, r.S0[1], B0[1], ri, tv));
-        s = dadd(s, Pfull(r.em[o], k, nz, r.Sm[0], r.Sm[W], ri, tv));
-        s = dadd(s, Pfull(r.ep[o], k, nz, r.Sp[0], r.Sp[W], ri, tv));
+        double s = dadd(Pl(r.e0[o - 1], k, r.S0[-1], B0[-1]), Pl(r.e0[o + 1], k, r.S0[1], B0[1]));
+        s = dadd(s, Pl(r.em[o], k, r.Sm[0], r.Sm[W]));
+        s = dadd(s, Pl(r.ep[o], k, r.Sp[0], r.Sp[W]));
         double u;
         if (k == 1) u = dadd(dmul(d.c5, pc), dmul(dv, dadd(s, pn)));
         else if (k == nz) u = dadd(dmul(d.c5, pc), dmul(dv, dadd(s, pd)));
@@ -248,7 +251,7 @@ __device__ __forceinline__ void inter_generic(const IRow& r, double* out, double
 // in the reference's precedence (i ghosts first, weather.cpp:161-168, then j
 // ghosts, :152-159).  The cyclic partner comes from the slab, the far column
 // (fcol/fsp, element fsel) or -- for j ghosts -- global memory.
-template <int KP, bool DIST>
+template <int KP, bool DIST, bool PIN>
 __device__ __forceinline__ void inter_ghost(const IRow& r, double* out, double* ib, int kl, int nk,
                                             int gi, int jr, int cc, int i0, const Dom& d,
                                          const double* __restrict__ e,
@@ -278,23 +281,26 @@ __device__ __forceinline__ void inter_ghost(const IRow& r, double* out, double* 
         sff = DIST ? __ldcg(sf + gi + jf * d.s2j) : __ldg(sf + gi + jf * d.s2j);
         pbf = DIST ? __ldcg(pb + gi + jf * d.s2j) : __ldg(pb + gi + jf * d.s2j);
     }
+    auto Pl = [&](double x, int k, double sfv, double pbv) {
+        return PIN ? x : Pfull(x, k, nz, sfv, pbv, ri, tv);
+    };
 #pragma unroll
     for (int kk = 0; kk < KP; ++kk) {
         if (kk >= nk) break;
         const int k = kl + kk;
         const int o = (k - 1) * W;
-        const double pg = Pfull(r.e0[o], k, nz, r.S0[0], B0[0], ri, tv);
+        const double pg = Pl(r.e0[o], k, r.S0[0], B0[0]);
         double a, b;
         if (ig) {
-            const double pf = Pfull(fcol[(k - 1) * 2 + fsel], k, nz, fsp[fsel], fsp[2 + fsel], ri, tv);
-            a = in1 ? Pfull(e0b[o + c1], k, nz, s0b[c1], b0b[c1], ri, tv) : pf; // P(1)
-            b = inn ? Pfull(e0b[o + cn], k, nz, s0b[cn], b0b[cn], ri, tv) : pf; // P(nx)
+            const double pf = Pl(fcol[(k - 1) * 2 + fsel], k, fsp[fsel], fsp[2 + fsel]);
+            a = in1 ? Pl(e0b[o + c1], k, s0b[c1], b0b[c1]) : pf; // P(1)
+            b = inn ? Pl(e0b[o + cn], k, s0b[cn], b0b[cn]) : pf; // P(nx)
         } else {
             const double* pe = ef + (long long)(k - 1) * d.sk;
-            const double pf = Pfull(DIST ? __ldcg(pe) : __ldg(pe), k, nz, sff, pbf, ri, tv);
+            const double pf = Pl(DIST ? __ldcg(pe) : __ldg(pe), k, sff, pbf);
             // jr = 0: P(ny) far, P(1) = row jr+1; jr = ny+1: P(ny) = row jr-1, P(1) far
-            a = jr == 0 ? pf : Pfull(r.em[o], k, nz, r.Sm[0], r.Sm[W], ri, tv);
-            b = jr == 0 ? Pfull(r.ep[o], k, nz, r.Sp[0], r.Sp[W], ri, tv) : pf;
+            a = jr == 0 ? pf : Pl(r.em[o], k, r.Sm[0], r.Sm[W]);
+            b = jr == 0 ? Pl(r.ep[o], k, r.Sp[0], r.Sp[W]) : pf;
         }
         const double u = dadd(dmul(d.c2, pg), dmul(dv, dadd(a, b)));
         const double v = Pfull(u, k, nz, r.S0[0], B0[0], ri, tv);
@@ -308,10 +314,22 @@ __device__ __forceinline__ void inter_ghost(const IRow& r, double* out, double* 
 // neighbours and the j+1 neighbour from registers (Pc = row j, Pn = row j+1,
 // both this thread's column); only the k neighbours across the group's ends
 // come from B0.  weather.cpp:130-150 on P'.
-template <int NK, bool FIRST, bool LAST>
+// POUT: store the post-physics value P(e_{s+2}) (the next pass reads it as it
+// is, PIN); sfj / pbj: sf and pb of this column at row j (planes 1 / nz).
+template <bool POUT>
+__device__ __forceinline__ double pout(double v, bool top, bool bot, double sfj, double pbj,
+                                       const Dom& d) {
+    if (!POUT) return v;
+    double p = dadd(v, d.ri);
+    if (top) p = dsub(p, dmul(d.tv, dsub(p, sfj)));
+    if (bot) p = dsub(p, dmul(d.tv, dsub(p, pbj)));
+    return p;
+}
+
+template <int NK, bool FIRST, bool LAST, bool POUT>
 __device__ __forceinline__ void final_smem(const double* Bm, const double* B0, const double* Pc,
                                            const double* Pn, double* q, long long sk, int kl,
-                                           bool store, const Dom& d) {
+                                           bool store, double sfj, double pbj, const Dom& d) {
     const double dv = d.dv, c6 = d.c6, c5 = d.c5;
     const int o0 = (kl - 1) * kPairIC;
     Bm += o0;
@@ -331,14 +349,17 @@ __device__ __forceinline__ void final_smem(const double* Bm, const double* B0, c
     }
     if (store) {
 #pragma unroll
-        for (int kk = 0; kk < NK; ++kk) q[(long long)kk * sk] = v[kk];
+        for (int kk = 0; kk < NK; ++kk)
+            q[(long long)kk * sk] =
+                pout<POUT>(v[kk], FIRST && kk == 0, LAST && kk == NK - 1, sfj, pbj, d);
     }
 }
 
-template <int KP>
+template <int KP, bool POUT>
 __device__ __forceinline__ void final_smem_generic(const double* Bm, const double* B0,
                                                    const double* Bp, double* q, long long sk,
-                                                   int kl, int nk, const Dom& d) {
+                                                   int kl, int nk, double sfj, double pbj,
+                                                   const Dom& d) {
     const int nz = d.nz;
     const double dv = d.dv;
 #pragma unroll
@@ -353,7 +374,7 @@ __device__ __forceinline__ void final_smem_generic(const double* Bm, const doubl
         if (k == 1) v = dadd(dmul(d.c5, B0[o]), dmul(dv, dadd(s, B0[o + kPairIC])));
         else if (k == nz) v = dadd(dmul(d.c5, B0[o]), dmul(dv, dadd(s, B0[o - kPairIC])));
         else v = dadd(dmul(d.c6, B0[o]), dmul(dv, dadd(dadd(s, B0[o - kPairIC]), B0[o + kPairIC])));
-        q[(long long)kk * sk] = v;
+        q[(long long)kk * sk] = pout<POUT>(v, k == 1, k == nz, sfj, pbj, d);
     }
 }
 
@@ -379,8 +400,11 @@ __device__ __forceinline__ void pair_publish(const double* v, int kl, int nk, in
 // The second producer of a chunk's i-ghost intermediates computes that
 // chunk's i-ghost cells of e_{s+2} (rows ja..jb, plus 0 / ny+1 at the domain
 // ends): weather.cpp:164-167 on the intermediate field.
+template <bool POUT>
 __device__ __forceinline__ void pair_ghost_cols(const Dom& d, const PairArgs& a,
-                                             double* __restrict__ u, int ja, int jb, int tid) {
+                                             double* __restrict__ u, const double* __restrict__ sf,
+                                             const double* __restrict__ pb, int ja, int jb,
+                                             int tid) {
     const int nx = d.nx, ny = d.ny, nz = d.nz;
     const int r0 = ja == 1 ? 0 : ja, r1 = jb == ny ? ny + 1 : jb;
     const int nr = r1 - r0 + 1;
@@ -395,15 +419,20 @@ __device__ __forceinline__ void pair_ghost_cols(const Dom& d, const PairArgs& a,
         const int side = (int)(q / nr); // 0: i = 0, 1: i = nx+1
         const double pg = G(side == 0 ? 0 : 3, j, k);
         const double v = dadd(dmul(d.c2, pg), dmul(d.dv, dadd(G(1, j, k), G(2, j, k))));
-        u[(side == 0 ? 0 : nx + 1) * d.si + j * d.sj + (long long)(k - 1) * d.sk] = v;
+        const int i = side == 0 ? 0 : nx + 1;
+        u[i * d.si + j * d.sj + (long long)(k - 1) * d.sk] =
+            POUT ? pout<true>(v, k == 1, k == nz, __ldg(sf + i + j * d.s2j), __ldg(pb + i + j * d.s2j), d)
+                 : v;
     }
 }
 
 // The second producer of a strip's j-ghost intermediates computes that
 // strip's j-ghost cells (i in i0..i0+TX-1 clipped to 1..nx, j = 0 and ny+1):
 // weather.cpp:155-158 on the intermediate field.
+template <bool POUT>
 __device__ __forceinline__ void pair_ghost_rows(const Dom& d, const PairArgs& a,
-                                             double* __restrict__ u, int i0, int tid) {
+                                             double* __restrict__ u, const double* __restrict__ sf,
+                                             const double* __restrict__ pb, int i0, int tid) {
     const int nx = d.nx, ny = d.ny, nz = d.nz;
     const int ni = min(kPairTX, nx - i0 + 1);
     const long long n = 2LL * ni * nz;
@@ -417,7 +446,10 @@ __device__ __forceinline__ void pair_ghost_rows(const Dom& d, const PairArgs& a,
         const int side = (int)(q / nz); // 0: j = 0, 1: j = ny+1
         const double pg = G(side == 0 ? 0 : 3, i, k);
         const double v = dadd(dmul(d.c2, pg), dmul(d.dv, dadd(G(2, i, k), G(1, i, k))));
-        u[i * d.si + (side == 0 ? 0 : ny + 1) * d.sj + (long long)(k - 1) * d.sk] = v;
+        const int j = side == 0 ? 0 : ny + 1;
+        u[i * d.si + j * d.sj + (long long)(k - 1) * d.sk] =
+            POUT ? pout<true>(v, k == 1, k == nz, __ldg(sf + i + j * d.s2j), __ldg(pb + i + j * d.s2j), d)
+                 : v;
     }
 }
 
@@ -492,7 +524,11 @@ struct RingPos {
 
 // KPT: max k planes per thread (nz <= 8 * KPT).  DIST: a decomposed rank's
 // subdomain (a separate instantiation: the single-domain code is unchanged).
-template <int KPT, bool DIST>
+// PIN / POUT (single domain): e_s is stored post-physics / store e_{s+2}
+// post-physics -- between the passes of one call the field is kept as P(e),
+// which is all the next pass reads, so no pass but the first recomputes the
+// physics of its loads (the same rounded ops, done once by the producer).
+template <int KPT, bool DIST, bool PIN, bool POUT>
 __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
     step_pair_kernel(const __grid_constant__ CUtensorMap tm_e,
                      const __grid_constant__ CUtensorMap tm_sfpb,
@@ -605,20 +641,20 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
                 const bool ghost = DIST ? ig || (d.own_s && jr == 0) || (d.own_n && jr == ny + 1)
                                         : ig || jr == 0 || jr == ny + 1;
                 switch (ghost ? 16 : shape) {
-                case 0: inter_inner<KPT, KPT, false, false>(r, PW2, ibrow, kl, d); break;
-                case 4: inter_inner<KPT, KPT - 1, false, false>(r, PW2, ibrow, kl, d); break;
-                case 5: inter_inner<KPT, KPT - 1, true, false>(r, PW2, ibrow, kl, d); break;
-                case 6: inter_inner<KPT, KPT - 1, false, true>(r, PW2, ibrow, kl, d); break;
+                case 0: inter_inner<KPT, KPT, false, false, PIN>(r, PW2, ibrow, kl, d); break;
+                case 4: inter_inner<KPT, KPT - 1, false, false, PIN>(r, PW2, ibrow, kl, d); break;
+                case 5: inter_inner<KPT, KPT - 1, true, false, PIN>(r, PW2, ibrow, kl, d); break;
+                case 6: inter_inner<KPT, KPT - 1, false, true, PIN>(r, PW2, ibrow, kl, d); break;
                 default:
                     if (ghost) {
                         const unsigned char* sb = s0_ - cc * 8;
                         const double* fb = reinterpret_cast<const double*>(sb + G.slab + G.sfpb);
                         const double* fsp =
                             reinterpret_cast<const double*>(sb + G.slab + G.sfpb + G.fcol);
-                        inter_ghost<KPT, DIST>(r, PW2, ibrow, kl, nk, gi, jr, cc, i0, d, e, sf, pb, fb,
+                        inter_ghost<KPT, DIST, PIN>(r, PW2, ibrow, kl, nk, gi, jr, cc, i0, d, e, sf, pb, fb,
                                          fsp, fsel);
                     } else {
-                        inter_generic<KPT>(r, PW2, ibrow, kl, nk, d);
+                        inter_generic<KPT, PIN>(r, PW2, ibrow, kl, nk, d);
                     }
                     break;
                 }
@@ -629,6 +665,10 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
                     if (owns_j) pair_publish<KPT>(PW2, kl, nk, gi, jr, d, a);
                 }
             }
+            // POUT: sf / pb of row jr-1 (the final row's planes 1 / nz) before its slab is freed
+            double sfj = 0.0, pbj = 0.0;
+            if (POUT && kfirst) sfj = reinterpret_cast<const double*>(sm_ + G.slab)[0];
+            if (POUT && klast) pbj = reinterpret_cast<const double*>(sm_ + G.slab)[kPairW];
             __syncthreads(); // intermediate row jr complete; slab jr-1 free
             // refill slab jr-1's slot (and, after the last row, those of jb+1, jb+2)
             if (tid == 0) {
@@ -644,11 +684,11 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
                 const double* Bp = ib0 + ibi * ibn + (cc - 1);
                 double* q = qrow;
                 switch (shape) {
-                case 0: final_smem<KPT, false, false>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d); break;
-                case 4: final_smem<KPT - 1, false, false>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d); break;
-                case 5: final_smem<KPT - 1, true, false>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d); break;
-                case 6: final_smem<KPT - 1, false, true>(Bm, B0, PW1, PW2, q, d.sk, kl, true, d); break;
-                default: final_smem_generic<KPT>(Bm, B0, Bp, q, d.sk, kl, nk, d); break;
+                case 0: final_smem<KPT, false, false, POUT>(Bm, B0, PW1, PW2, q, d.sk, kl, true, sfj, pbj, d); break;
+                case 4: final_smem<KPT - 1, false, false, POUT>(Bm, B0, PW1, PW2, q, d.sk, kl, true, sfj, pbj, d); break;
+                case 5: final_smem<KPT - 1, true, false, POUT>(Bm, B0, PW1, PW2, q, d.sk, kl, true, sfj, pbj, d); break;
+                case 6: final_smem<KPT - 1, false, true, POUT>(Bm, B0, PW1, PW2, q, d.sk, kl, true, sfj, pbj, d); break;
+                default: final_smem_generic<KPT, POUT>(Bm, B0, Bp, q, d.sk, kl, nk, sfj, pbj, d); break;
                 }
             }
             // No second barrier: the next row's target buffer (ib2) is read here only
@@ -693,8 +733,8 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
             }
             __syncthreads();
             const int f = s_flags;
-            if (f & 1) pair_ghost_cols(d, a, u, ja, jb, tid);
-            if (f & 2) pair_ghost_rows(d, a, u, i0, tid);
+            if (f & 1) pair_ghost_cols<POUT>(d, a, u, sf, pb, ja, jb, tid);
+            if (f & 2) pair_ghost_rows<POUT>(d, a, u, sf, pb, i0, tid);
             __syncthreads(); // s_flags is reused by the next rim unit
         }
     }
