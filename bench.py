@@ -510,6 +510,8 @@ def run_ours(args):
             if n_gpus == 1:
                 line["e2e_run"] = e2e_run(ctx, cfg, args, stream)
                 line["output_path"] = output_path(ctx, cfg, ms_per_step)
+    if args.workload == "stencil":
+        line["multi_sweep"] = multi_sweep(ctx, K, stream, inner, alg_bytes, peak)
     if rank == 0 and n_gpus == 1 and not args.no_cpu_baseline:
         rate, dt, kind, sample = cpu_reference_rate(grid, args.cpu_steps, args.workload)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": 1, "kind": kind,
@@ -525,6 +527,31 @@ def run_ours(args):
     if dist is not None:
         dist.destroy_process_group()
     return 0
+
+
+def multi_sweep(ctx, K, stream, inner, alg_bytes, peak):
+    """The stencil workload's K sweeps as ONE hftw_diffuse_steps(K) call on one grid
+    (the multi-step schedule: sweep s+1 starts on the rows sweep s has finished),
+    after an L2 flush, best of 3.  The grid's two 34 MB fields stay in the 126 MB L2
+    between its sweeps, so this is not an HBM-bound figure (the main line is: every
+    sweep's input there is L2-cold)."""
+    import torch
+    best = None
+    for _ in range(3):
+        ctx.flush_l2(256 << 20)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        ctx.diffuse(K)
+        b.record(stream)
+        b.synchronize()
+        ms = a.elapsed_time(b) / K
+        best = ms if best is None else min(best, ms)
+    return {"sweeps_per_call": K, "ms_per_sweep": best, "value": inner / (best * 1e-3),
+            "unit": UNIT, "algorithmic_GBps": alg_bytes / (best * 1e-3) / 1e9,
+            "algorithmic_frac_of_copy_peak": alg_bytes / (best * 1e-3) / 1e9 / peak,
+            "gpu_launches": 1,
+            "note": "one persistent launch of K sweeps after an L2 flush; the 2 x 34 MB "
+                    "working set stays L2-resident between sweeps (not HBM-bound)"}
 
 
 def e2e(ctx, sim, cfg, args, stream, world):

@@ -190,6 +190,9 @@ int hftw_physics(hftw_ctx* ctx, int mode);
 /* Phases 2-5 alone (weather.cpp:130-168): ENERGY <- diffusion(ENERGY), with
  * ENERGY_U receiving the previous ENERGY (the swap of weather.cpp:170). */
 int hftw_diffuse(hftw_ctx* ctx);
+/* n diffusion-only sweeps (n x hftw_diffuse, bitwise): one persistent launch
+ * whose sweeps overlap as a wavefront (the multi-step schedule of hftw_step). */
+int hftw_diffuse_steps(hftw_ctx* ctx, int64_t n);
 
 /* Measurement hook: overwrite `bytes` of scratch device memory on the context
  * stream (evicts the L2 between timed sweeps) with the same shared-memory

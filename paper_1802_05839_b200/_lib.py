@@ -92,6 +92,7 @@ SIGNATURES = [
     ("hftw_get_kernel", C.c_int, [_P]),
     ("hftw_physics", C.c_int, [_P, C.c_int]),
     ("hftw_diffuse", C.c_int, [_P]),
+    ("hftw_diffuse_steps", C.c_int, [_P, C.c_int64]),
     ("hftw_flush_l2", C.c_int, [_P, C.c_size_t]),
     ("hftw_algorithmic_bytes", C.c_double, [_P, C.c_int]),
     ("hftw_launches_per_step", C.c_int, [_P]),

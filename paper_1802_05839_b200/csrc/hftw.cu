@@ -502,7 +502,12 @@ using PairKernel = void (*)(const CUtensorMap, const CUtensorMap, const CUtensor
 constexpr int kPairIn = 1, kPairOut = 2;
 PairKernel pair_kernel(bool dist, int form = 0) {
     using namespace hftw;
-    if (dist) return step_pair_kernel<kPairKPT, true, false, false>;
+    if (dist) switch (form) {
+        case kPairIn: return step_pair_kernel<kPairKPT, true, true, false>;
+        case kPairOut: return step_pair_kernel<kPairKPT, true, false, true>;
+        case kPairIn | kPairOut: return step_pair_kernel<kPairKPT, true, true, true>;
+        default: return step_pair_kernel<kPairKPT, true, false, false>;
+        }
     switch (form) {
     case kPairIn: return step_pair_kernel<kPairKPT, false, true, false>;
     case kPairOut: return step_pair_kernel<kPairKPT, false, false, true>;
@@ -547,7 +552,7 @@ int setup_pair(hftw_ctx* c) {
     if (!ns) return HFTW_OK;
     c->pair_ns = ns;
     c->pair_smem = hftw::pair_smem_bytes(nz, ns);
-    for (int form = 0; form < (c->dist ? 1 : 4); ++form)
+    for (int form = 0; form < 4; ++form)
         CUDA_TRY(c, raise_smem_attr((const void*)pair_kernel(c->dist, form), c->pair_smem));
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, hftw::kPairThreads,
@@ -672,7 +677,7 @@ int launch_pair(hftw_ctx* c, int src, int form) {
     const Halo h = make_halo(c, src ^ 1); // pushes into the neighbours' e_{s+2}, waits >= s
     int rc = timing_mark(c, 1, true);
     if (rc) return rc;
-    auto kern = pair_kernel(c->dist, c->dist ? 0 : form);
+    auto kern = pair_kernel(c->dist, form);
     kern<<<c->pair_ctas, hftw::kPairThreads, c->pair_smem, c->stream>>>(
         c->tm_e2[src], c->tm_sfpb, c->tm_ef[src], c->tm_sfpbf, e3(c, src), e3(c, src ^ 1), sf2(c),
         pb2(c), d, a, h);
@@ -683,7 +688,7 @@ int launch_pair(hftw_ctx* c, int src, int form) {
 // Decomposed pair pass, second launch: the ghost cells of e_{s+2} from this
 // rank's and the wrap partners' published P', their pushes, and the release
 // of the pass to every neighbour (weather_pair.cuh, pair_ghost_kernel).
-int launch_pair_ghost(hftw_ctx* c, int dst) {
+int launch_pair_ghost(hftw_ctx* c, int dst, int form) {
     const Dom d = make_dom(c);
     Halo h = make_halo(c, dst);
     h.step = c->step_count + 1; // releases s + 2
@@ -717,7 +722,12 @@ int launch_pair_ghost(hftw_ctx* c, int dst) {
     const int blocks = (int)std::max<long long>(
         1, std::min<long long>((cells + 1023) / 1024,
                                (long long)env_int("HFTW_GHOST_CTAS", c->num_sms / 2)));
-    hftw::pair_ghost_kernel<<<blocks, 256, 0, c->stream>>>(e3(c, dst), d, h, g);
+    if (form & kPairOut)
+        hftw::pair_ghost_kernel<true><<<blocks, 256, 0, c->stream>>>(e3(c, dst), sf2(c), pb2(c),
+                                                                     d, h, g);
+    else
+        hftw::pair_ghost_kernel<false><<<blocks, 256, 0, c->stream>>>(e3(c, dst), sf2(c), pb2(c),
+                                                                      d, h, g);
     CUDA_TRY(c, cudaGetLastError());
     return HFTW_OK;
 }
@@ -731,11 +741,16 @@ int64_t pair_passes(int64_t nsteps) { return nsteps / 2; }
 // One pass: phase bit 0 launches the pair kernel, bit 1 (decomposed) the ghost
 // kernel, and then the bookkeeping.  A group on one device runs bit 0 for every
 // rank before bit 1 for any (the ghost kernels wait for the wrap partners').
-int pair_pass(hftw_ctx* c, int phase, int form = 0) {
+// Storage form of pass p of `pairs` (pair_kernel): post-physics in between.
+int pair_form(int64_t p, int64_t pairs) {
+    return (p > 0 ? kPairIn : 0) | (p + 1 < pairs ? kPairOut : 0);
+}
+
+int pair_pass(hftw_ctx* c, int phase, int form) {
     int rc;
     if ((phase & 1) && (rc = launch_pair(c, c->cur, form))) return rc;
     if (phase & 2) {
-        if (c->dist && (rc = launch_pair_ghost(c, c->cur ^ 1))) return rc;
+        if (c->dist && (rc = launch_pair_ghost(c, c->cur ^ 1, form))) return rc;
         c->cur ^= 1;
         c->step_count += 2;
         ++c->pass_count;
@@ -752,8 +767,9 @@ int pair_pass(hftw_ctx* c, int phase, int form = 0) {
 int setup_wave(hftw_ctx* c) {
     c->wave_ok = false;
     if (!c->tma_ok || c->layout != HFTW_IJK || c->tx != 64) return HFTW_OK;
-    auto kern = hftw::step_wave_kernel<64, kNCW>;
+    auto kern = hftw::step_wave_kernel<64, kNCW, true>;
     CUDA_TRY(c, raise_smem_attr((const void*)kern, c->smem));
+    CUDA_TRY(c, raise_smem_attr((const void*)hftw::step_wave_kernel<64, kNCW, false>, c->smem));
     int per_sm = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, (kNCW + 1) * 32, c->smem) !=
             cudaSuccess ||
@@ -803,8 +819,9 @@ int setup_wave(hftw_ctx* c) {
     return HFTW_OK;
 }
 
-// nsteps single steps in ONE launch (buf[src] holds the field of step 0).
-int launch_wave(hftw_ctx* c, int src, int64_t nsteps) {
+// nsteps single steps in ONE launch (buf[src] holds the field of step 0);
+// phys = false: diffusion-only sweeps.
+int launch_wave(hftw_ctx* c, int src, int64_t nsteps, bool phys = true) {
     Dom d = make_dom(c);
     hftw::WaveArgs a{};
     a.fp = kFrontPad;
@@ -826,7 +843,8 @@ int launch_wave(hftw_ctx* c, int src, int64_t nsteps) {
     a.step_done = c->d_wave + 2 + c->wave_nchunks + 1;
     int rc = timing_mark(c, 2, true);
     if (rc) return rc;
-    hftw::step_wave_kernel<64, kNCW><<<c->wave_ctas, (kNCW + 1) * 32, c->smem, c->stream>>>(
+    auto kern = phys ? hftw::step_wave_kernel<64, kNCW, true> : hftw::step_wave_kernel<64, kNCW, false>;
+    kern<<<c->wave_ctas, (kNCW + 1) * 32, c->smem, c->stream>>>(
         c->tm_e[src], c->tm_e[src ^ 1], c->tm_sf, c->tm_pb, sf2(c), pb2(c), d, a);
     CUDA_TRY(c, cudaGetLastError());
     return timing_mark(c, 2, false, nsteps);
@@ -1380,7 +1398,7 @@ int group_step(hftw_ctx* c, int64_t nsteps) {
                 for (int phase : {1, 2})
                     for (hftw_ctx* r : c->ranks) {
                         RANK_TRY(c, r, check_ctx(r));
-                        RANK_TRY(c, r, pair_pass(r, phase));
+                        RANK_TRY(c, r, pair_pass(r, phase, pair_form(p, pairs)));
                     }
             nsteps -= 2 * pairs;
         }
@@ -1738,13 +1756,11 @@ int hftw_step(hftw_ctx* c, int64_t nsteps) {
         // pairs, then one or two single steps: the last step is a single-step
         // launch so that energy_u (physics of the field before it) stays
         // derivable from the ping-pong partner
-        // single domain: between the passes of this call the field is stored
-        // post-physics (the first pass reads, the last one writes, plain e)
+        // between the passes of this call the field is stored post-physics (the
+        // first pass reads, the last one writes, plain e)
         const int64_t pairs = pair_passes(nsteps);
-        for (int64_t p = 0; p < pairs; ++p) {
-            const int form = c->dist ? 0 : (p > 0 ? kPairIn : 0) | (p + 1 < pairs ? kPairOut : 0);
-            if ((rc = pair_pass(c, 3, form))) return rc;
-        }
+        for (int64_t p = 0; p < pairs; ++p)
+            if ((rc = pair_pass(c, 3, pair_form(p, pairs)))) return rc;
         nsteps -= 2 * pairs;
     }
     const bool multistep = c->opt_multistep > 0 || (c->opt_multistep == 0 && c->wave_pref);
@@ -1967,6 +1983,38 @@ int hftw_diffuse(hftw_ctx* c) {
     c->eu_stored = false;
     c->eu_pending = false;
     c->cur ^= 1;
+    return HFTW_OK;
+}
+
+int hftw_diffuse_steps(hftw_ctx* c, int64_t n) {
+    NvtxRange nvtx_("hftw_diffuse_steps");
+    int rc = check_ctx(c);
+    if (rc) return rc;
+    if (c->dist || is_group(c))
+        return fail(c, HFTW_EUNSUP, "diffusion-only sweeps are single-domain");
+    if ((rc = check_state(c))) return rc;
+    if (n < 0) return fail(c, HFTW_EINVAL, "sweeps must be nonnegative");
+    if (n == 0) return HFTW_OK;
+    if (n == 1 || !c->wave_ok) {
+        for (int64_t s = 0; s < n; ++s)
+            if ((rc = hftw_diffuse(c))) return rc;
+        return HFTW_OK;
+    }
+    // all sweeps in persistent launches of the multi-step schedule (the field
+    // of sweep s+1 is read as soon as the rows it needs from sweep s are done)
+    for (int64_t left = n; left > 0;) {
+        const int64_t m = std::min<int64_t>(left, (int64_t)1 << 20);
+        if (m == 1) {
+            if ((rc = hftw_diffuse(c))) return rc;
+            break;
+        }
+        if ((rc = launch_wave(c, c->cur, m, false))) return rc;
+        if (m & 1) c->cur ^= 1;
+        left -= m;
+    }
+    c->eu_derived = false; // energy_u = the last sweep's input (swap semantics)
+    c->eu_stored = false;
+    c->eu_pending = false;
     return HFTW_OK;
 }
 

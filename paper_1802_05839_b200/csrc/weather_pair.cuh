@@ -524,7 +524,7 @@ struct RingPos {
 
 // KPT: max k planes per thread (nz <= 8 * KPT).  DIST: a decomposed rank's
 // subdomain (a separate instantiation: the single-domain code is unchanged).
-// PIN / POUT (single domain): e_s is stored post-physics / store e_{s+2}
+// PIN / POUT: e_s is stored post-physics / store e_{s+2}
 // post-physics -- between the passes of one call the field is kept as P(e),
 // which is all the next pass reads, so no pass but the first recomputes the
 // physics of its loads (the same rounded ops, done once by the producer).
@@ -778,8 +778,11 @@ struct PairGhostArgs {
     long long pub;        // the value it releases (s + 2)
 };
 
-__global__ void __launch_bounds__(256) pair_ghost_kernel(double* __restrict__ u, Dom d, Halo h,
-                                                         PairGhostArgs g) {
+template <bool POUT>
+__global__ void __launch_bounds__(256) pair_ghost_kernel(double* __restrict__ u,
+                                                         const double* __restrict__ sf,
+                                                         const double* __restrict__ pb, Dom d,
+                                                         Halo h, PairGhostArgs g) {
     const int nx = d.nx, ny = d.ny, nz = d.nz;
     if (threadIdx.x == 0 && !h.nowait) {
         for (int q = 0; q < 4; ++q)
@@ -835,8 +838,12 @@ __global__ void __launch_bounds__(256) pair_ghost_kernel(double* __restrict__ u,
                          dmul(d.dv, dadd(R(g.grow, 2, i, k), R(g.grow_n, 1, i, k))));
             }
         }
-        u[i * d.si + j * d.sj + (long long)(k - 1) * d.sk] = v;
-        halo_push(h, d, i, j, k, v);
+        // POUT: stored (and pushed) post-physics, like the pair kernel's cells
+        const double w = POUT ? pout<true>(v, k == 1, k == nz, __ldg(sf + i + j * d.s2j),
+                                           __ldg(pb + i + j * d.s2j), d)
+                              : v;
+        u[i * d.si + j * d.sj + (long long)(k - 1) * d.sk] = w;
+        halo_push(h, d, i, j, k, w);
     }
     __syncthreads();
     if (threadIdx.x == 0) halo_signal(h);

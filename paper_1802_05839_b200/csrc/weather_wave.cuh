@@ -75,6 +75,7 @@ __device__ __forceinline__ bool wave_rows_down(const WaveArgs& a, int unit) {
 
 // One ghost-row task: its share of rows j = 0 and ny+1 (all i, corners
 // included; cell_update applies the reference's precedence).
+template <bool PHYS>
 __device__ __forceinline__ void wave_ghost_rows(const double* __restrict__ e,
                                                 double* __restrict__ u,
                                                 const double* __restrict__ sf,
@@ -94,13 +95,14 @@ __device__ __forceinline__ void wave_ghost_rows(const double* __restrict__ e,
         const long long q = t / ni;
         const int k = 1 + (int)(q % d.nz);
         const int j = ((q / d.nz) == 0 && d.own_s) ? 0 : d.ny + 1;
-        const double v = cell_update<true, true>(e, sf, pb, d, i, j, k);
+        const double v = cell_update<PHYS, true>(e, sf, pb, d, i, j, k);
         u[i * d.si + j * d.sj + (long long)(k - 1) * d.sk] = v;
         halo_push(h, d, i, j, k, v);
     }
 }
 
 // i-ghost columns of rows ja..jb: i = 0 (strip 0) and/or nx+1 (last strip).
+template <bool PHYS>
 __device__ __forceinline__ void wave_ghost_cols(const double* __restrict__ e,
                                                 double* __restrict__ u,
                                                 const double* __restrict__ sf,
@@ -116,7 +118,7 @@ __device__ __forceinline__ void wave_ghost_cols(const double* __restrict__ e,
         const int j = ja + (int)(q % nr);
         const int k = 1 + (int)(q / nr);
         const int i = w ? 0 : d.nx + 1;
-        const double v = cell_update<true, true>(e, sf, pb, d, i, j, k);
+        const double v = cell_update<PHYS, true>(e, sf, pb, d, i, j, k);
         u[i * d.si + j * d.sj + (long long)(k - 1) * d.sk] = v;
         halo_push(h, d, i, j, k, v); // a ghost column's first / last rows go to S / N
     }
@@ -136,7 +138,7 @@ __device__ __forceinline__ void wave_item_done(const WaveArgs& a, int s, int per
 }
 
 // Consumer warps of step_wave_kernel (the row loop of step_tma_kernel).
-template <int TX, int NCW>
+template <int TX, int NCW, bool PHYS>
 __device__ __forceinline__ void wave_consumers(unsigned char* smem, const SlabGeom& G,
                                                uint64_t* full, uint64_t* empty,
                                                const int* slot_item,
@@ -177,7 +179,7 @@ __device__ __forceinline__ void wave_consumers(unsigned char* smem, const SlabGe
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[L % NS]);
             ++L;
-            wave_ghost_rows(e, u, sf, pb, d, (s & 1) ? a.h_odd : a.h_even, r, a.gtasks, tid,
+            wave_ghost_rows<PHYS>(e, u, sf, pb, d, (s & 1) ? a.h_odd : a.h_even, r, a.gtasks, tid,
                             nthreads);
             asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
             if (tid == 0) {
@@ -217,7 +219,7 @@ __device__ __forceinline__ void wave_consumers(unsigned char* smem, const SlabGe
                              (long long)(kl - 1) * d.sk;
                 const ColumnRow row{em, e0, ep, Sm, S0, Sp, Bm, B0, Bp, up, d.sk,
                                     w, 1, kl, kh, nz, ri, tv, dv, c5, c6, i0 + c, j};
-                column_row<true>(row);
+                column_row<PHYS>(row);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[l0 % NS]);
@@ -236,7 +238,7 @@ __device__ __forceinline__ void wave_consumers(unsigned char* smem, const SlabGe
         }
         // the i-ghost columns of these rows (their partners are in the same rows)
         const bool west = st == 0 && d.own_w, east = st == a.nstrips - 1 && d.own_e;
-        if (west || east) wave_ghost_cols(e, u, sf, pb, d, hs, ja, jb, west, east, tid, nthreads);
+        if (west || east) wave_ghost_cols<PHYS>(e, u, sf, pb, d, hs, ja, jb, west, east, tid, nthreads);
         // publish: every consumer's stores of this unit precede the count
         asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
         if (tid == 0) {
@@ -248,7 +250,9 @@ __device__ __forceinline__ void wave_consumers(unsigned char* smem, const SlabGe
     }
 }
 
-template <int TX, int NCW>
+// PHYS = false: diffusion-only sweeps of an already post-physics field
+// (hftw_diffuse_steps), the same schedule.
+template <int TX, int NCW, bool PHYS>
 __global__ void __launch_bounds__((NCW + 1) * 32, 1)
     step_wave_kernel(const __grid_constant__ CUtensorMap tm_e0,
                      const __grid_constant__ CUtensorMap tm_e1,
@@ -358,7 +362,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
         }
         __syncwarp();
     } else {
-        wave_consumers<TX, NCW>(smem, G, full, empty, slot_item, sf, pb, d, a);
+        wave_consumers<TX, NCW, PHYS>(smem, G, full, empty, slot_item, sf, pb, d, a);
     }
     // every warp of this CTA is done (consumers have published their units):
     // the last CTA to finish re-arms the scheduler and the counters

@@ -314,8 +314,13 @@ class Context:
     def physics(self, mode: int = 0) -> None:
         self._chk(lib().hftw_physics(self._h, mode))
 
-    def diffuse(self) -> None:
-        self._chk(lib().hftw_diffuse(self._h))
+    def diffuse(self, n: int = 1) -> None:
+        """n diffusion-only sweeps (phases 2-5 of reference_step); n > 1 runs them as
+        one persistent multi-sweep launch (hftw_diffuse_steps)."""
+        if n == 1:
+            self._chk(lib().hftw_diffuse(self._h))
+        else:
+            self._chk(lib().hftw_diffuse_steps(self._h, int(n)))
 
     def sync(self) -> None:
         self._chk(lib().hftw_sync(self._h))

@@ -163,6 +163,30 @@ def test_diffusion_sweep_vs_oracle(coracle, shape):
     assert bad.size == 0, (shape, bad[:5])
 
 
+@pytest.mark.parametrize("shape,n", [((256, 256, 64), 2), ((256, 256, 64), 7), ((37, 20, 17), 4),
+                                     ((70, 9, 33), 3), ((130, 200, 8), 5)])
+def test_diffusion_sweeps_vs_oracle(coracle, shape, n):
+    """n diffusion-only sweeps in one call (hftw_diffuse_steps: one multi-sweep
+    launch where the grid allows it) = n single sweeps of the oracle, bitwise; energy_u
+    is the last sweep's input (the swap)."""
+    nx, ny, nz = shape
+    rng = np.random.default_rng(nx + 7 * ny + 31 * nz + n)
+    cfg = W.GridConfig(nx=nx, ny=ny, nz=nz, diffusion_velocity=float(rng.uniform(0, 1 / 6)))
+    g = O.grid_from(cfg)
+    n3, _ = O.shapes(g)
+    e = rng.uniform(150, 350, n3)
+    want, prev = e.copy(), None
+    for _ in range(n):
+        prev, want = want, coracle.diffuse(g, want.copy())
+    with W.Context(cfg) as ctx:
+        ctx.upload("energy", e)
+        ctx.diffuse(n)
+        got, got_u = ctx.download("energy"), ctx.download("energy_u")
+    for a, b, f in ((got, want, "energy"), (got_u, prev, "energy_u")):
+        bad = np.flatnonzero(a.view(np.uint64) != b.view(np.uint64))
+        assert bad.size == 0, (shape, n, f, bad[:5])
+
+
 def test_energy_u_observability(coracle):
     """energy_u after a step is the post-physics, pre-diffusion field
     (weather.cpp:118-128 in place, then the swap at :170)."""

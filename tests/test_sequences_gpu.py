@@ -54,7 +54,7 @@ def sequences(n=120, seed=int(os.environ.get("HFTW_FUZZ_SEED", "1802"))):
             elif r < 0.55:
                 ops.append(("physics", int(rng.integers(0, 2))))
             elif r < 0.65:
-                ops.append(("diffuse",))
+                ops.append(("diffuse", int(rng.integers(1, 4))))
             elif r < 0.8:
                 ops.append(("upload", str(rng.choice(FIELDS))))
             else:
@@ -91,8 +91,9 @@ def test_call_sequence_vs_oracle(coracle, seq):
                 ctx.physics(op[1])
                 m.physics()
             elif op[0] == "diffuse":
-                ctx.diffuse()
-                m.diffuse()
+                ctx.diffuse(op[1])
+                for _ in range(op[1]):
+                    m.diffuse()
             elif op[0] == "upload":
                 new = rng.uniform(150, 350, n3 if op[1] in ("energy", "energy_u") else n2)
                 ctx.upload(op[1], new)
