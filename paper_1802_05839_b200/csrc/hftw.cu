@@ -596,13 +596,14 @@ int setup_pair(hftw_ctx* c) {
     const long long slots = (long long)per_sm * c->num_sms;
     if (chunk <= 0) {
         // Rows per unit by how many waves of 16-row units a pass has (measured with
-        // tools/group_diag.py and HFTW_PAIR_CHUNK, profiles/r02_chunk_sweep.txt):
-        // >= 5 waves 16 rows (ASUCA, 14.7 waves: 0.519 ms per pass vs 0.534 at 12 and
-        // 0.554 at 8 -- longer units also lose, to the launch tail), 2.5-5 waves 12
+        // tools/group_diag.py, tools/ab_step.py and HFTW_PAIR_CHUNK / _CHUNK2,
+        // profiles/r02_chunk_sweep.txt): >= 5 waves 24 rows (ASUCA, 14.7 waves, with
+        // post-physics storage between passes: 0.2431 ms/step vs 0.2493 at 16, 0.2461
+        // at 32 and 0.2559 at 12, each with half-height tail units), 2.5-5 waves 12
         // (a 2x2 rank: 0.187 vs 0.192 at 16), fewer 8 (a 2x4 rank: 0.122 vs 0.133):
         // short passes need more units to fill both CTAs of every SM.
         const double w16 = (double)((long long)c->pair_nstrips * ((ny + 15) / 16)) / (double)slots;
-        chunk = w16 >= 5.0 ? 16 : w16 >= 2.5 ? 12 : 8;
+        chunk = w16 >= 5.0 ? 24 : w16 >= 2.5 ? 12 : 8;
     }
     c->pair_chunk = (int)std::min<long long>(chunk, ny);
     // the last ~1.5 waves of units get half-height chunks (a shorter tail)
