@@ -19,6 +19,7 @@ for layout in ("ijk", "kij"):
             ctx.physics(0)
             ctx.physics(1)
             ctx.diffuse()
+            ctx.diffuse(3)
             st = ctx.download_state()
             e, eu = ctx.step_host(st.energy.data.copy(), st.energy_surf.data.copy(),
                                   st.energy_pbl.data.copy())
