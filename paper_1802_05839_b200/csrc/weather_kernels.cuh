@@ -235,11 +235,12 @@ __device__ __forceinline__ void push_box(const Halo& h, const Dom& d, const doub
                                          int i1, int j0, int j1, int tid, int nthr) {
     // the box's columns / rows next to a face: 0..2 and n-1..n+1, up to six when
     // the box spans both faces (a whole owned box, or a narrow subdomain)
+    // (the two ranges directly: a scan of the box would cost O(width) per thread)
     int cs[6], rs[6], nc = 0, nr = 0;
-    for (int i = i0; i <= i1 && nc < 6; ++i)
-        if (i <= 2 || i >= d.nx - 1) cs[nc++] = i;
-    for (int j = j0; j <= j1 && nr < 6; ++j)
-        if (j <= 2 || j >= d.ny - 1) rs[nr++] = j;
+    for (int i = i0; i <= min(i1, 2); ++i) cs[nc++] = i;
+    for (int i = max(i0, max(d.nx - 1, 3)); i <= i1; ++i) cs[nc++] = i;
+    for (int j = j0; j <= min(j1, 2); ++j) rs[nr++] = j;
+    for (int j = max(j0, max(d.ny - 1, 3)); j <= j1; ++j) rs[nr++] = j;
     const int nj = j1 - j0 + 1, ni = i1 - i0 + 1;
     const long long a = (long long)nc * nj;       // face columns x all rows
     const long long b = (long long)nr * ni;       // face rows x all columns (dups skipped)
