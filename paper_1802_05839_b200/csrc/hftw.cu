@@ -522,6 +522,8 @@ PairKernel pair_kernel(bool dist, int form = 0) {
 int setup_pair(hftw_ctx* c) {
     c->pair_ok = false;
     if (!c->tma_ok || c->layout != HFTW_IJK || c->nz > hftw::kPairKG * kPairKPT) return HFTW_OK;
+    // the kernel's final-row stores index planes with int offsets (kk * plane stride)
+    if ((long long)kPairKPT * c->Pi * c->Rows > 0x7fffffffLL) return HFTW_OK;
     if (c->dist) {
         // every rank of the decomposition must take the same decision: two-step
         // passes need 2 owned cells next to every interior face of every rank

@@ -328,7 +328,7 @@ __device__ __forceinline__ double pout(double v, bool top, bool bot, double sfj,
 
 template <int NK, bool FIRST, bool LAST, bool POUT>
 __device__ __forceinline__ void final_smem(const double* Bm, const double* B0, const double* Pc,
-                                           const double* Pn, double* q, long long sk, int kl,
+                                           const double* Pn, double* q, int sk, int kl,
                                            bool store, double sfj, double pbj, const Dom& d) {
     const double dv = d.dv, c6 = d.c6, c5 = d.c5;
     const int o0 = (kl - 1) * kPairIC;
@@ -350,14 +350,14 @@ __device__ __forceinline__ void final_smem(const double* Bm, const double* B0, c
     if (store) {
 #pragma unroll
         for (int kk = 0; kk < NK; ++kk)
-            q[(long long)kk * sk] =
+            q[kk * sk] =
                 pout<POUT>(v[kk], FIRST && kk == 0, LAST && kk == NK - 1, sfj, pbj, d);
     }
 }
 
 template <int KP, bool POUT>
 __device__ __forceinline__ void final_smem_generic(const double* Bm, const double* B0,
-                                                   const double* Bp, double* q, long long sk,
+                                                   const double* Bp, double* q, int sk,
                                                    int kl, int nk, double sfj, double pbj,
                                                    const Dom& d) {
     const int nz = d.nz;
@@ -374,7 +374,7 @@ __device__ __forceinline__ void final_smem_generic(const double* Bm, const doubl
         if (k == 1) v = dadd(dmul(d.c5, B0[o]), dmul(dv, dadd(s, B0[o + kPairIC])));
         else if (k == nz) v = dadd(dmul(d.c5, B0[o]), dmul(dv, dadd(s, B0[o - kPairIC])));
         else v = dadd(dmul(d.c6, B0[o]), dmul(dv, dadd(dadd(s, B0[o - kPairIC]), B0[o + kPairIC])));
-        q[(long long)kk * sk] = pout<POUT>(v, k == 1, k == nz, sfj, pbj, d);
+        q[kk * sk] = pout<POUT>(v, k == 1, k == nz, sfj, pbj, d);
     }
 }
 
@@ -577,6 +577,9 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
         }
     }
     const int kh = kl + nk - 1;
+    // plane stride as an int: kk * sk stays below 2^31 (setup_pair checks KPT * sk), so
+    // the final's store addresses are one 32 x 32 + 64 multiply-add each
+    const int sk32 = (int)d.sk;
     const bool kfirst = kl == 1, klast = kh == nz;
     // compile-time row shapes: nk in {KPT, KPT-1} x (first, last); else generic
     const int fl = (kfirst ? 1 : 0) + (klast ? 2 : 0);
@@ -684,11 +687,11 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
                 const double* Bp = ib0 + ibi * ibn + (cc - 1);
                 double* q = qrow;
                 switch (shape) {
-                case 0: final_smem<KPT, false, false, POUT>(Bm, B0, PW1, PW2, q, d.sk, kl, true, sfj, pbj, d); break;
-                case 4: final_smem<KPT - 1, false, false, POUT>(Bm, B0, PW1, PW2, q, d.sk, kl, true, sfj, pbj, d); break;
-                case 5: final_smem<KPT - 1, true, false, POUT>(Bm, B0, PW1, PW2, q, d.sk, kl, true, sfj, pbj, d); break;
-                case 6: final_smem<KPT - 1, false, true, POUT>(Bm, B0, PW1, PW2, q, d.sk, kl, true, sfj, pbj, d); break;
-                default: final_smem_generic<KPT, POUT>(Bm, B0, Bp, q, d.sk, kl, nk, sfj, pbj, d); break;
+                case 0: final_smem<KPT, false, false, POUT>(Bm, B0, PW1, PW2, q, sk32, kl, true, sfj, pbj, d); break;
+                case 4: final_smem<KPT - 1, false, false, POUT>(Bm, B0, PW1, PW2, q, sk32, kl, true, sfj, pbj, d); break;
+                case 5: final_smem<KPT - 1, true, false, POUT>(Bm, B0, PW1, PW2, q, sk32, kl, true, sfj, pbj, d); break;
+                case 6: final_smem<KPT - 1, false, true, POUT>(Bm, B0, PW1, PW2, q, sk32, kl, true, sfj, pbj, d); break;
+                default: final_smem_generic<KPT, POUT>(Bm, B0, Bp, q, sk32, kl, nk, sfj, pbj, d); break;
                 }
             }
             // No second barrier: the next row's target buffer (ib2) is read here only
