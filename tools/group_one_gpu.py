@@ -6,7 +6,7 @@ run -- minus the NVLink cost of its halo pushes, which the in-kernel push
 overlaps with compute.  Strong scaling: the ASUCA grid split px x py; weak: an
 ASUCA-sized subdomain per rank.  Prints one JSON line per decomposition with
 the per-rank ms/step and the implied efficiency against the 1-GPU run.
-usage: group_one_gpu.py [K]"""
+usage: group_one_gpu.py [K] [PXxPY,... strong process grids]"""
 import json
 import os
 import sys
@@ -31,9 +31,13 @@ def timed(ctx, k):
     return a.elapsed_time(b) / k
 
 
+CASES = ((1, 1, "-"), (2, 1, "strong"), (2, 2, "strong"), (2, 4, "strong"),
+         (2, 1, "weak"), (2, 2, "weak"), (2, 4, "weak"))
+if len(sys.argv) > 2:  # other process grids, strong: e.g. 4x2,8x1,1x8
+    CASES = ((1, 1, "-"),) + tuple((int(g.split("x")[0]), int(g.split("x")[1]), "strong")
+                                   for g in sys.argv[2].split(","))
 base = None
-for px, py, scaling in ((1, 1, "-"), (2, 1, "strong"), (2, 2, "strong"), (2, 4, "strong"),
-                        (2, 1, "weak"), (2, 2, "weak"), (2, 4, "weak")):
+for px, py, scaling in CASES:
     n = px * py
     nx, ny = (1581 * px, 1301 * py) if scaling == "weak" else (1581, 1301)
     cfg = W.GridConfig(nx=nx, ny=ny, nz=58)
