@@ -10,7 +10,8 @@
 // result is bitwise identical to two reference steps.
 //
 // Tiling (IJK store, two persistent 256-thread CTAs per SM, dynamic j-major
-// work units of 30-column strips x 16 rows, the last ~1.5 waves of units 8 rows):
+// work units of 30-column strips x 24 rows at ASUCA size, the last ~1.5 waves of
+// units half as tall; 12 / 8-row units on small decomposed domains):
 //   * per row j, ONE TMA box of e_s covers columns i0-2 .. i0+31 and all k,
 //     one box the sf and pb rows, and -- for the two edge strips -- a 2-wide
 //     box holds the cyclic partner column of the i-ghost cell (column nx for
