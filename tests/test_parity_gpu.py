@@ -73,12 +73,15 @@ def test_golden_cases(golden, layout, kernel):
 
 @pytest.mark.parametrize("layout", LAYOUTS)
 def test_auto_kernel_selected(layout):
-    # AUTO: two-step passes (IJK, one domain, 56 <= nz <= 58: the compile-time row
-    # shapes); the TMA kernel otherwise (fused_pair still runs other nz on request)
+    # AUTO: two-step passes (IJK, one domain, 50 <= nz <= 58: the compile-time row
+    # shapes of 10 k-groups of 5-6 planes); the TMA kernel otherwise (fused_pair still
+    # runs other nz on request)
     with W.Context(W.GridConfig(nx=100, ny=40, nz=58), layout=layout) as ctx:
         assert ctx.kernel == ("fused_pair" if layout == "ijk" else "fused_tma")
         assert ctx.launches_per_step == 1
     with W.Context(W.GridConfig(nx=100, ny=40, nz=50), layout=layout) as ctx:
+        assert ctx.kernel == ("fused_pair" if layout == "ijk" else "fused_tma")
+    with W.Context(W.GridConfig(nx=100, ny=40, nz=49), layout=layout) as ctx:
         assert ctx.kernel == "fused_tma"
         if layout == "ijk":
             ctx.set_kernel("fused_pair")
