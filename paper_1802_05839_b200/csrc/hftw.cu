@@ -783,16 +783,17 @@ int setup_wave(hftw_ctx* c) {
     // Long units: the launch's tail is paid once per call, not once per step,
     // and fewer chunk boundaries mean fewer halo rows re-read from HBM -- but a
     // step needs enough units to keep every CTA busy while the previous step's
-    // rows complete.  The longest of 32/24/16/12/8 rows that gives >= 2.4 units
-    // per CTA per step (tools/wave_chunk_sweep.py: ASUCA 32 rows; the 1/4 and 1/8
-    // ranks of the 2x2 / 2x4 decompositions 24 and 12 rows, 7% and 27% faster
-    // per step than 32).
+    // rows complete.  The longest of 32/24/16/12/8/6 rows that gives >= 2.4 units
+    // per CTA per step, else 4 (tools/wave_chunk_sweep.py: ASUCA 32 rows; the 1/4 and
+    // 1/8 ranks of the 2x2 / 2x4 decompositions 24 and 12 rows, 7% and 27% faster
+    // per step than 32; the 256x256x64 diffusion sweeps 4 rows: 14.4 us per sweep
+    // against 17.0 at 8 and 16.6 at 2, tools/gpu_r2ae.sh).
     const long long ny = c->lny;
     long long chunk = env_int("HFTW_WAVE_CHUNK", 0);
     if (chunk <= 0) {
         const long long slots = (long long)per_sm * c->num_sms;
-        chunk = 8;
-        for (long long cand : {32LL, 24LL, 16LL, 12LL}) {
+        chunk = 4;
+        for (long long cand : {32LL, 24LL, 16LL, 12LL, 8LL, 6LL}) {
             if ((long long)c->nstrips * ((ny + cand - 1) / cand) * 10 >= slots * 24) {
                 chunk = cand;
                 break;
