@@ -1402,7 +1402,12 @@ int group_step(hftw_ctx* c, int64_t nsteps) {
                 for (int phase : {1, 2})
                     for (hftw_ctx* r : c->ranks) {
                         RANK_TRY(c, r, check_ctx(r));
-                        RANK_TRY(c, r, pair_pass(r, phase, pair_form(p, pairs)));
+                        const int rc = pair_pass(r, phase, pair_form(p, pairs));
+                        if (rc) {
+                            // ranks already past earlier passes hold post-physics fields
+                            for (hftw_ctx* q : c->ranks) q->poisoned = 0xF;
+                            return rank_fail(c, r, rc);
+                        }
                     }
             nsteps -= 2 * pairs;
         }
@@ -1764,7 +1769,12 @@ int hftw_step(hftw_ctx* c, int64_t nsteps) {
         // first pass reads, the last one writes, plain e)
         const int64_t pairs = pair_passes(nsteps);
         for (int64_t p = 0; p < pairs; ++p)
-            if ((rc = pair_pass(c, 3, pair_form(p, pairs)))) return rc;
+            if ((rc = pair_pass(c, 3, pair_form(p, pairs)))) {
+                // a pass failed after earlier passes left the field post-physics: the
+                // state is not the reference's any more
+                if (p > 0) c->poisoned = 0xF;
+                return rc;
+            }
         nsteps -= 2 * pairs;
     }
     const bool multistep = c->opt_multistep > 0 || (c->opt_multistep == 0 && c->wave_pref);
