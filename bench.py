@@ -137,12 +137,14 @@ def layout_plan(args, n):
     grid, desc = WORKLOADS[args.workload]
     nx, ny, nz = grid
     px, py = (args.px, args.py) if args.px else process_grid(n)
-    scaling = "weak" if n == 1 else args.scaling
+    # at n = 1 strong and weak are the same run; the label follows --scaling so that
+    # every line of a scaling series carries the same one
+    scaling = args.scaling
     if n > 1 and scaling == "weak":
         nx, ny = nx * px, ny * py  # every GPU keeps an ASUCA-sized subdomain
-        desc = f"full timestep, weak: {nx}x{ny}x{nz} fp64 on {px}x{py} (ASUCA per GPU)"
+        desc = f"full step weak {nx}x{ny}x{nz} f64 {px}x{py}"
     elif n > 1:
-        desc = f"full timestep, strong: ASUCA {nx}x{ny}x{nz} fp64 on {px}x{py}"
+        desc = f"full step strong {nx}x{ny}x{nz} f64 {px}x{py}"
     return px, py, scaling, (nx, ny, nz), desc
 
 
