@@ -494,6 +494,25 @@ int setup_tma(hftw_ctx* c) {
     return HFTW_OK;
 }
 
+// A launch that may start while the previous one on the stream finishes (programmatic
+// dependent launch; the kernel waits for it before touching global memory), or a
+// plain launch when HFTW_PDL is 0.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t stream, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = HFTW_PDL ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 using PairKernel = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap,
                            const CUtensorMap, const double*, double*, const double*,
                            const double*, Dom, hftw::PairArgs, const Halo);
@@ -681,9 +700,10 @@ int launch_pair(hftw_ctx* c, int src, int form) {
     int rc = timing_mark(c, 1, true);
     if (rc) return rc;
     auto kern = pair_kernel(c->dist, form);
-    kern<<<c->pair_ctas, hftw::kPairThreads, c->pair_smem, c->stream>>>(
-        c->tm_e2[src], c->tm_sfpb, c->tm_ef[src], c->tm_sfpbf, e3(c, src), e3(c, src ^ 1), sf2(c),
-        pb2(c), d, a, h);
+    CUDA_TRY(c, launch_pdl(kern, c->pair_ctas, hftw::kPairThreads, c->pair_smem, c->stream,
+                           c->tm_e2[src], c->tm_sfpb, c->tm_ef[src], c->tm_sfpbf,
+                           (const double*)e3(c, src), e3(c, src ^ 1), (const double*)sf2(c),
+                           (const double*)pb2(c), d, a, h));
     CUDA_TRY(c, cudaGetLastError());
     return timing_mark(c, 1, false, 2);
 }
@@ -848,8 +868,9 @@ int launch_wave(hftw_ctx* c, int src, int64_t nsteps, bool phys = true) {
     int rc = timing_mark(c, 2, true);
     if (rc) return rc;
     auto kern = phys ? hftw::step_wave_kernel<64, kNCW, true> : hftw::step_wave_kernel<64, kNCW, false>;
-    kern<<<c->wave_ctas, (kNCW + 1) * 32, c->smem, c->stream>>>(
-        c->tm_e[src], c->tm_e[src ^ 1], c->tm_sf, c->tm_pb, sf2(c), pb2(c), d, a);
+    CUDA_TRY(c, launch_pdl(kern, c->wave_ctas, (kNCW + 1) * 32, c->smem, c->stream, c->tm_e[src],
+                           c->tm_e[src ^ 1], c->tm_sf, c->tm_pb, (const double*)sf2(c),
+                           (const double*)pb2(c), d, a));
     CUDA_TRY(c, cudaGetLastError());
     return timing_mark(c, 2, false, nsteps);
 }
@@ -911,8 +932,9 @@ int launch_fused(hftw_ctx* c, int src, int kernel, const StepPart* part = nullpt
         const int ctas = (int)std::max<long long>(1, std::min<long long>(c->ctas, want));
         dim3 block((kNCW + 1) * 32);
 #define HFTW_LAUNCH_TMA(TX, KIJ)                                                              \
-    hftw::step_tma_kernel<TX, kNCW, PHYS, KIJ><<<ctas, block, c->smem, c->stream>>>(         \
-        c->tm_e[src], c->tm_sf, c->tm_pb, e3(c, src), dst, sf2(c), pb2(c), d, a, h)
+    launch_pdl(hftw::step_tma_kernel<TX, kNCW, PHYS, KIJ>, ctas, block, c->smem, c->stream,    \
+               c->tm_e[src], c->tm_sf, c->tm_pb, (const double*)e3(c, src), dst,              \
+               (const double*)sf2(c), (const double*)pb2(c), d, a, h)
         const bool kij = c->layout == HFTW_KIJ;
         if (c->tx == 64) {
             if (kij) HFTW_LAUNCH_TMA(64, true);

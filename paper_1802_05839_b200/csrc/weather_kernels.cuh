@@ -24,7 +24,23 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#ifndef HFTW_PDL
+#define HFTW_PDL 1
+#endif
+
 namespace hftw {
+
+// Programmatic dependent launch (the step kernels are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization): let the next launch on the
+// stream be scheduled now -- its CTAs take SMs as ours exit, so its launch and
+// prologue overlap our tail -- then wait until the previous launch has completed and
+// its writes are visible.  Called by every thread before any global memory access.
+__device__ __forceinline__ void pdl_start() {
+#if HFTW_PDL
+    asm volatile("griddepcontrol.launch_dependents;");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
 
 // Device-side description of one (sub)domain.  Logical indices follow the
 // reference: i in [0, nx+1], j in [0, ny+1], k in [1, nz]; the pointers
@@ -861,6 +877,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    pdl_start();
 
     if (warp == NCW) {
         // ---------------- producer: work scheduler + TMA issue ----------------

@@ -558,6 +558,7 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
     const int nx = d.nx, ny = d.ny, nz = d.nz;
 
     PairProducer prod{0, 1, -2, 0, false}; // row > jb + 2: the first issue takes a unit
+    pdl_start();
     if (tid == 0) {
         for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");

@@ -280,6 +280,7 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    pdl_start();
 
     if (warp == NCW) {
         // ---------------- producer: work list, dependency waits, TMA ----------------
