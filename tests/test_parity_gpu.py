@@ -370,6 +370,18 @@ def test_pair_kernel_is_auto_and_hash(golden, coracle):
         assert coracle.fnv(got[f]) == v, f
 
 
+@pytest.mark.parametrize("steps", [7, 20])
+def test_headline_run_vs_reference_hash(golden, coracle, steps):
+    """The bench's exact run on one GPU: init + hftw_step(steps) at 1581x1301x58 through
+    AUTO (pair passes, the field post-physics between them; 7 steps end with a single
+    step), bitwise against the unmodified reference's run_reference hashes -- energy_u
+    included (recomputed from a post-physics partner after 20 steps)."""
+    h = golden["hashes"][f"1581x1301x58_s{steps}"]
+    got = run_device(cfg_of(h["grid"]), steps, "ijk", "auto")
+    for f, v in h["fnv1a64"].items():
+        assert coracle.fnv(got[f]) == v, (steps, f)
+
+
 def test_pair_kernel_asuca_vs_oracle(coracle):
     """BASELINE's full size, 5 steps = 2 pairs + 1 single step, bitwise."""
     cfg = W.GridConfig(nx=1581, ny=1301, nz=58)
