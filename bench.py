@@ -47,6 +47,7 @@ WORKLOADS = {
 }
 
 
+SPEC_HBM_GBPS = 8000.0  # B200 HBM3e specification (report against it too)
 ROTATE = 6  # stencil workload: independent grids swept round robin
 
 
@@ -179,29 +180,42 @@ def cpu_reference_rate(grid, steps, workload="full"):
     import oracle as O
     nx, ny, nz = grid
     g = O.make_grid(nx, ny, nz)
-    kind = "port"
-    if workload == "full" and O.RefOracle.available():
-        kind = "reference"
-        dt = O.RefOracle().time_steps(g, steps)
-    else:
-        c = O.COracle()
-        st = c.init(g)
-        t0 = time.perf_counter()
-        if workload == "full":
-            c.lib.wo_steps(C_byref(g), steps, *(O._p(a) for a in (st.energy, st.energy_u,
-                                                                 st.energy_surf, st.energy_pbl)))
-        elif workload == "physics":
-            for _ in range(steps):
-                c.lib.wo_physics(C_byref(g), O._p(st.energy), O._p(st.energy_surf),
-                                 O._p(st.energy_pbl))
-        else:
-            for _ in range(steps):
-                c.lib.wo_diffuse(C_byref(g), O._p(st.energy), O._p(st.energy_u))
-        dt = time.perf_counter() - t0
+    # one pinned core: the calling thread runs the serial reference
+    allowed = sorted(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else []
+    cpu = allowed[-1] if allowed else None
+    if cpu is not None:
+        os.sched_setaffinity(0, {cpu})
+    try:
+        dt = _cpu_steps(O, g, steps, workload)
+        kind = "reference" if workload == "full" and O.RefOracle.available() else "port"
+    finally:
+        if cpu is not None:
+            os.sched_setaffinity(0, set(allowed))
     rate = nx * ny * nz * steps / dt
     what = "hft::reference_step (oracle/_ref)" if kind == "reference" else f"oracle port ({workload})"
-    sample = f"{steps} x {what} on {nx}x{ny}x{nz}: {dt:.2f} s, 1 thread (the reference is serial)"
+    sample = (f"{steps} x {what} on {nx}x{ny}x{nz}: {dt:.2f} s, 1 thread pinned to cpu {cpu} "
+              f"(the reference is serial)")
     return rate, dt, kind, sample
+
+
+def _cpu_steps(O, g, steps, workload):
+    """Seconds for `steps` of the reference CPU path (see cpu_reference_rate)."""
+    if workload == "full" and O.RefOracle.available():
+        return O.RefOracle().time_steps(g, steps)
+    c = O.COracle()
+    st = c.init(g)
+    t0 = time.perf_counter()
+    if workload == "full":
+        c.lib.wo_steps(C_byref(g), steps, *(O._p(a) for a in (st.energy, st.energy_u,
+                                                             st.energy_surf, st.energy_pbl)))
+    elif workload == "physics":
+        for _ in range(steps):
+            c.lib.wo_physics(C_byref(g), O._p(st.energy), O._p(st.energy_surf),
+                             O._p(st.energy_pbl))
+    else:
+        for _ in range(steps):
+            c.lib.wo_diffuse(C_byref(g), O._p(st.energy), O._p(st.energy_u))
+    return time.perf_counter() - t0
 
 
 def C_byref(x):
@@ -474,6 +488,8 @@ def run_ours(args):
             "effective_gbs": achieved,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "spec_peak": SPEC_HBM_GBPS, "spec_frac": achieved / SPEC_HBM_GBPS,
+                         "dram_spec_frac": dram / SPEC_HBM_GBPS if dram else None,
                          "dram_gbs": dram, "dram_frac": dram / peak if dram else None,
                          "per": "GPU (rank 0)" if n_gpus > 1 else "GPU",
                          "kernel": dom_name,
