@@ -63,7 +63,7 @@ constexpr int kPairW = kPairTX + 4;             // slab columns i0-2 .. i0+TX+1
 #define HFTW_PAIR_KG 10
 #endif
 // k-groups (warps) per strip: 10 (<= 6 planes each, 320 threads, 95 registers) ties 8
-// (<= 8 planes, 256 threads, 124 registers) at ASUCA size and is 3% faster on the
+// (<= 8 planes, 256 threads, 124 registers; the round-1 layout) at ASUCA size and is 3% faster on the
 // 790 x 325 subdomain of a 2x4 decomposition; 9 / 11 / 12 / 14 are slower
 constexpr int kPairKG = HFTW_PAIR_KG;
 constexpr int kPairThreads = kPairIC * kPairKG;

@@ -329,9 +329,11 @@ def test_step_host_after_device_steps(coracle):
 
 @pytest.mark.parametrize("shape", [(100, 37, 58), (64, 64, 2), (65, 3, 9), (2, 2, 2), (33, 200, 17),
                                    (129, 2, 64), (128, 70, 58), (191, 97, 31), (1, 1, 1),
-                                   # every k-group split with compile-time row shapes
-                                   # (nz 56-58), and the first nz past the smem budget
-                                   (70, 45, 56), (61, 33, 57), (95, 20, 59)])
+                                   # k-group splits with compile-time row shapes (10
+                                   # groups of 5-6 planes: nz 50-58), and the first nz
+                                   # past the smem budget
+                                   (70, 45, 56), (61, 33, 57), (90, 25, 50), (77, 31, 53),
+                                   (64, 40, 55), (95, 20, 59)])
 @pytest.mark.parametrize("steps", [3, 4, 5, 8])
 def test_pair_kernel_vs_oracle(coracle, shape, steps):
     """Two steps per pass (intermediate field on chip): bitwise against the oracle on
