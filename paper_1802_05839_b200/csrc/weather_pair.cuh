@@ -553,6 +553,7 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
     uint64_t* full =
         reinterpret_cast<uint64_t*>(smem + (size_t)NS * G.stage + kPairNIB * (size_t)G.ib);
     int* slot_unit = reinterpret_cast<int*>(full + NS);
+    const uint32_t full_u32 = smem_u32(full); // the ring barriers' shared-window address
     __shared__ int s_flags;
     const int tid = threadIdx.x;
     const int nx = d.nx, ny = d.ny, nz = d.nz;
@@ -601,7 +602,7 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
     RingPos R0{0, 0}; // ring position of the current unit's first slab (row ja-2)
     int ibi = 0;      // row buffer of the next intermediate row (rotates over kPairNIB)
     for (;;) {
-        mbar_wait(&full[R0.slot], R0.par);
+        mbar_wait_u32(full_u32 + 8u * R0.slot, R0.par);
         const int unit = slot_unit[R0.slot];
         if (unit < 0) break;
         const int ch = unit / a.nstrips, st = unit % a.nstrips;
@@ -635,9 +636,9 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
         // advanced one row per iteration
         double* qrow = u + (long long)gi * d.si + (long long)(ja - 2) * d.sj +
                        (long long)(kl - 1) * d.sk;
-        mbar_wait(&full[Rb.slot], Rb.par);
+        mbar_wait_u32(full_u32 + 8u * Rb.slot, Rb.par);
         for (int jr = ja - 1; jr <= jb + 1; ++jr) {
-            mbar_wait(&full[Rc.slot], Rc.par);
+            mbar_wait_u32(full_u32 + 8u * Rc.slot, Rc.par);
             // row buffers: jr -> ibi, jr-1 -> ibi-1, jr-2 -> ibi-2 (mod kPairNIB)
             const int ib1 = ibi == 0 ? kPairNIB - 1 : ibi - 1;
             const int ib2 = ib1 == 0 ? kPairNIB - 1 : ib1 - 1;
