@@ -540,11 +540,68 @@ def run_ours(args):
         sim.close()
     else:
         ctx.close()
+    if n_gpus > 1 and scaling == "strong" and args.workload == "full":
+        # the weak-scaling companion of BASELINE config 5 in the same run: an
+        # ASUCA-sized subdomain per GPU (px*1581 x py*1301 x 58), same kernels
+        line["weak_companion"] = weak_companion(args, px, py, ngroup, world, device, dist)
     if rank == 0:
         print(json.dumps(line))
     if dist is not None:
         dist.destroy_process_group()
     return 0
+
+
+def weak_companion(args, px, py, ngroup, world, device, dist):
+    """K steps on the weak-scaled grid (an ASUCA-sized subdomain per GPU), timed like the
+    main line: one hftw_step(K) per rank between CUDA events on its stream(s), barriers on
+    both sides, the max over ranks."""
+    import torch
+    from paper_1802_05839_b200 import weather as W
+    from paper_1802_05839_b200.dist import DistSimulation
+    (nx, ny, nz), _ = WORKLOADS["full"]
+    cfg = W.GridConfig(nx=nx * px, ny=ny * py, nz=nz)
+    sim = None
+    if ngroup > 1:
+        ctx = W.Context(cfg, layout=args.layout, kernel=args.kernel, px=px, py=py,
+                        devices=list(range(ngroup)))
+        ctx.init()
+        ranks = [ctx.rank_context(r) for r in range(ngroup)]
+        streams = [torch.cuda.ExternalStream(rc.stream, device=r) for r, rc in enumerate(ranks)]
+    else:
+        sim = DistSimulation(cfg, px, py, layout=args.layout, device=device, kernel=args.kernel)
+        sim.init()
+        ctx = sim.ctx
+        streams = [torch.cuda.ExternalStream(ctx.stream, device=device)]
+    K = args.steps
+    ctx.step(max(args.warmup, 2))
+    ctx.sync()
+    evs = []
+    if dist is not None:
+        dist.barrier()
+    for st in streams:
+        with torch.cuda.device(st.device):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            evs.append((a, b, st))
+    ctx.step(K)
+    for a, b, st in evs:
+        with torch.cuda.device(st.device):
+            b.record(st)
+    ctx.sync()
+    ms = max(a.elapsed_time(b) for a, b, _ in evs)
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    if sim is not None:
+        sim.close()
+    else:
+        ctx.close()
+    n = px * py
+    value = cfg.nx * cfg.ny * cfg.nz / (ms / K * 1e-3)
+    return {"grid": [cfg.nx, cfg.ny, cfg.nz], "parallelism": f"{px}x{py}", "steps": K,
+            "ms_per_step": ms / K, "value": value, "unit": UNIT, "per_gpu_value": value / n,
+            "scaling": "weak"}
 
 
 def multi_sweep(ctx, K, stream, inner, alg_bytes, peak):
