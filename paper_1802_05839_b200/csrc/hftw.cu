@@ -968,15 +968,16 @@ int launch_physics(hftw_ctx* c, double* e, int mode) {
     Dom d = make_dom(c);
     const long long cols = (c->lnx + 2) * (c->lny + 2);
     if (mode == 0) {
-        hftw::physics_column_kernel<<<grid_for(c, cols), 256, 0, c->stream>>>(e, sf2(c),
-                                                                             pb2(c), d);
+        CUDA_TRY(c, launch_pdl(hftw::physics_column_kernel, grid_for(c, cols), 256, 0, c->stream,
+                               e, (const double*)sf2(c), (const double*)pb2(c), d));
     } else if (c->layout == HFTW_KIJ) {
         if (c->Pk >= 32 && env_int("HFTW_KIJ_PHYS_WARP", 0) == 0) { // streaming rows
             const long long tasks = (c->lny + 2) * ((c->lnx + 2 + 15) / 16);
-            hftw::physics_kij_stream_kernel<<<(int)std::min<long long>((tasks + 7) / 8,
-                                                                       (long long)c->num_sms * 16),
-                                              256, 0, c->stream>>>(e, sf2(c), pb2(c), d,
-                                                                   (int)c->Pk);
+            CUDA_TRY(c, launch_pdl(hftw::physics_kij_stream_kernel,
+                                   (int)std::min<long long>((tasks + 7) / 8,
+                                                            (long long)c->num_sms * 16),
+                                   256, 0, c->stream, e, (const double*)sf2(c),
+                                   (const double*)pb2(c), d, (int)c->Pk));
             CUDA_TRY(c, cudaGetLastError());
             return HFTW_OK;
         }

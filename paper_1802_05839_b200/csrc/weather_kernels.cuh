@@ -405,6 +405,7 @@ __global__ void __launch_bounds__(256) physics_column_kernel(double* __restrict_
                                                              const double* __restrict__ sf,
                                                              const double* __restrict__ pb,
                                                              Dom d) {
+    pdl_start();
     Owned o = owned(d);
     const int ni = o.i1 - o.i0 + 1, nj = o.j1 - o.j0 + 1;
     const long long n = (long long)ni * nj;
@@ -456,6 +457,7 @@ __global__ void __launch_bounds__(256) physics_kij_stream_kernel(double* __restr
                                                                  const double* __restrict__ sf,
                                                                  const double* __restrict__ pb,
                                                                  Dom d, int pk) {
+    pdl_start();
     constexpr int CPW = 16; // columns per warp task
     const Owned o = owned(d);
     const int ni = o.i1 - o.i0 + 1, nj = o.j1 - o.j0 + 1;
