@@ -163,10 +163,15 @@ enum hftw_option {
     HFTW_OPT_MULTISTEP = 1, /* single-step kernel, n >= 2 steps in ONE persistent launch:
                                -1 never, 0 where a step is short (default), 1 always */
     HFTW_OPT_PAIR = 2,      /* AUTO may use two-step passes: 1 (default) or 0 */
-    HFTW_OPT_EXCHANGE = 3   /* group contexts: 0 the step kernels push the halos (default);
+    HFTW_OPT_EXCHANGE = 3,  /* group contexts: 0 the step kernels push the halos (default);
                                1 the un-overlapped baseline -- steps without the halo
                                protocol, then a separate face-copy kernel per rank and
                                event waits (single-step kernels only; measurement) */
+    HFTW_OPT_REVERSE = 4    /* 1: the pair and single-step kernels hand out their work
+                               units in reverse order (last chunk first) -- the analogue
+                               of the reference emulator's launch-order reversal
+                               (interpreter.hpp:38-45), a race check: results must not
+                               change.  0 (default): the j-major order */
 };
 int hftw_set_option(hftw_ctx* ctx, int option, int64_t value);
 

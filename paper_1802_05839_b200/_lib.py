@@ -18,7 +18,7 @@ FIELDS = {"energy": HFTW_ENERGY, "energy_u": HFTW_ENERGY_U,
 LAYOUTS = {"ijk": 0, "kij": 1}
 KERNELS = {"auto": 0, "fused_tma": 1, "fused_cell": 2, "split": 3, "fused_pair": 4}
 KERNEL_NAMES = {v: k for k, v in KERNELS.items()}
-OPTIONS = {"multistep": 1, "pair": 2, "exchange": 3}  # enum hftw_option
+OPTIONS = {"multistep": 1, "pair": 2, "exchange": 3, "reverse": 4}  # enum hftw_option
 ERRORS = {0: "ok", 1: "EINVAL", 2: "ECUDA", 3: "ENOMEM", 4: "ESTATE", 5: "EUNSUP"}
 
 

@@ -168,6 +168,7 @@ struct hftw_ctx {
     bool wave_pref = false;     // multi-step launch preferred over one launch per step (auto)
     int opt_multistep = 0;      // HFTW_OPT_MULTISTEP: -1 never, 0 auto (wave_pref), 1 always
     int opt_exchange = 0;       // HFTW_OPT_EXCHANGE (groups): 0 in-kernel pushes, 1 baseline
+    int opt_reverse = 0;        // HFTW_OPT_REVERSE: work units handed out last first
     cudaEvent_t xev = nullptr;  // the baseline's "my faces are out" event
     int* d_wave = nullptr;      // sched[2] + chunk_done[nchunks] + ghost_done[1]
 
@@ -691,6 +692,7 @@ int launch_pair(hftw_ctx* c, int src, int form) {
     a.chunk2 = c->pair_chunk2;
     a.ns = c->pair_ns;
     a.sched = c->d_pair;
+    a.reverse = c->opt_reverse;
     a.cnt_col = c->d_pair + 2;
     a.cnt_row = c->d_pair + 2 + c->pair_nchunks;
     double* pub = gpub_of(c->gpub, c->gpub_n, c->pass_count);
@@ -904,6 +906,7 @@ hftw::TmaArgs tma_args(const hftw_ctx* c, const StepPart& p) {
     a.pk = (int)c->Pk;
     a.ghost_cells = ghost;
     a.sched = c->d_sched;
+    a.reverse = c->opt_reverse;
     a.u_lo = p.u_lo;
     a.u_hi = p.u_hi;
     a.gi_lo = p.gi_lo;
@@ -1985,6 +1988,10 @@ int hftw_set_option(hftw_ctx* c, int opt, int64_t v) {
     case HFTW_OPT_EXCHANGE:
         if (v != 0 && v != 1) return fail(c, HFTW_EINVAL, "HFTW_OPT_EXCHANGE takes 0 or 1");
         c->opt_exchange = (int)v;
+        return HFTW_OK;
+    case HFTW_OPT_REVERSE:
+        if (v != 0 && v != 1) return fail(c, HFTW_EINVAL, "HFTW_OPT_REVERSE takes 0 or 1");
+        c->opt_reverse = (int)v;
         return HFTW_OK;
     }
     return fail(c, HFTW_EINVAL, "unknown option %d", opt);

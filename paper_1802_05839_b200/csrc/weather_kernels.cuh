@@ -769,6 +769,7 @@ struct TmaArgs {
     int pk;        // KIJ column pitch (doubles)
     long long ghost_cells;
     int* sched;    // [0] next work unit, [1] CTAs finished (self-resetting)
+    int reverse;   // HFTW_OPT_REVERSE: hand the units out last first
     // Sub-range launches (hftw_step_host pipelines a step in row blocks):
     // units [u_lo, u_hi) of the j-major order, the i-ghost columns of rows
     // [gi_lo, gi_hi] (clipped to the owned inner rows) and the j-ghost rows
@@ -901,8 +902,9 @@ __global__ void __launch_bounds__((NCW + 1) * 32, 1)
             uint32_t L = 0;
             long long seen = -1; // the step whose neighbour flags this producer has seen
             for (;;) {
-                const int unit = a.u_lo + atomicAdd(&a.sched[0], 1);
-                const bool stop = unit >= a.u_hi;
+                const int v = atomicAdd(&a.sched[0], 1);
+                const bool stop = v >= a.u_hi - a.u_lo;
+                const int unit = a.reverse ? a.u_hi - 1 - v : a.u_lo + v;
                 int ja = 0, jb = -1, ic = 0;
                 if (!stop) {
                     const int ch = unit / a.nstrips, st = unit % a.nstrips;

@@ -111,6 +111,7 @@ struct PairArgs {
     int nbig;     // chunks 0 .. nbig-1 have `chunk` rows, the rest `chunk2` (the last
     int chunk2;   // ~1.5 waves of units are shorter, so the launch's tail is shorter)
     int* sched;   // [0] next unit, [1] CTAs finished (self-resetting)
+    int reverse;  // HFTW_OPT_REVERSE: hand the units out last first
     int* cnt_col; // [nchunks] i-ghost producers done (strip 0 + last strip), self-resetting
     int* cnt_row; // [nstrips] j-ghost producers done (chunk 0 + last chunk), self-resetting
     double* gcol; // P' at i = 0, 1, nx, nx+1: [4][ny+2][nz]
@@ -482,6 +483,7 @@ __device__ __forceinline__ void pair_issue(PairProducer& p, unsigned char* smem,
     if (p.row > p.jb + 2) {
         // the current unit is fully issued: take the next one
         p.unit = atomicAdd(&a.sched[0], 1);
+        if (a.reverse && p.unit < a.nstrips * a.nchunks) p.unit = a.nstrips * a.nchunks - 1 - p.unit;
         if (p.unit >= a.nstrips * a.nchunks) {
             slot_unit[slot] = -1;
             mbar_arrive(&full[slot]); // no bytes: tells the consumers to finish

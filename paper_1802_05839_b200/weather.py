@@ -340,7 +340,8 @@ class Context:
         self._chk(lib().hftw_set_kernel(self._h, L.KERNELS[name]))
 
     def set_option(self, name: str, value: int) -> None:
-        """hftw_set_option: "multistep" (-1 never, 0 auto, 1 always) or "pair" (0/1)."""
+        """hftw_set_option: "multistep" (-1 never, 0 auto, 1 always), "pair" (0/1),
+        "exchange" (groups: 0/1) or "reverse" (0/1: work units handed out last first)."""
         self._chk(lib().hftw_set_option(self._h, L.OPTIONS[name], int(value)))
 
     @property

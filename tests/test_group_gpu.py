@@ -170,6 +170,21 @@ def test_asuca_default_path_vs_reference_hash(golden, coracle):
                 assert coracle.fnv(ctx.download(f)) == v, (steps, f)
 
 
+def test_group_reverse_unit_order_bitwise(coracle):
+    """Decomposed pair passes and single steps with the work units handed out last
+    first (HFTW_OPT_REVERSE) on every rank: bitwise."""
+    cfg = W.GridConfig(nx=150, ny=97, nz=58, diffusion_velocity=0.11)
+    s0 = random_state(cfg, 17)
+    want = coracle.steps(O.grid_from(cfg), s0, 7).fields()
+    with group(cfg, 2, 2) as ctx:
+        for f, a in s0.fields().items():
+            ctx.upload(f, np.ascontiguousarray(a))
+        ctx.set_option("reverse", 1)
+        ctx.step(7)
+        got = {f: ctx.download(f) for f in FIELDS}
+    assert_bitwise(got, want, "2x2 reverse")
+
+
 @pytest.mark.parametrize("grid", [(2, 1), (2, 2), (2, 4)])
 def test_exchange_baseline_bitwise(coracle, grid):
     """HFTW_OPT_EXCHANGE = 1 (the un-overlapped baseline: steps without the halo

@@ -384,6 +384,24 @@ def test_headline_run_vs_reference_hash(golden, coracle, steps):
         assert coracle.fnv(got[f]) == v, (steps, f)
 
 
+@pytest.mark.parametrize("shape,kernel", [((150, 97, 58), "auto"), ((133, 61, 51), "auto"),
+                                          ((150, 97, 58), "fused_tma"), ((70, 200, 17), "fused_tma")])
+def test_reverse_unit_order_bitwise(coracle, shape, kernel):
+    """HFTW_OPT_REVERSE (the work units handed out last chunk first; the analogue of the
+    reference emulator's launch-order reversal, interpreter.hpp:38-45) gives the same
+    bits: no result depends on the order in which CTAs take their units."""
+    nx, ny, nz = shape
+    cfg = W.GridConfig(nx=nx, ny=ny, nz=nz, diffusion_velocity=0.13)
+    rng = np.random.default_rng(nx + nz)
+    g = O.grid_from(cfg)
+    n3, n2 = O.shapes(g)
+    s0 = O.State(rng.uniform(150, 350, n3), rng.uniform(150, 350, n3),
+                 rng.uniform(150, 350, n2), rng.uniform(150, 350, n2))
+    want = coracle.steps(g, s0, 6).fields()
+    got = run_device(cfg, 6, "ijk", kernel, s0.fields(), options={"reverse": 1, "multistep": -1})
+    assert_same(got, want, f"{shape}/{kernel}/reverse")
+
+
 def test_pair_kernel_asuca_vs_oracle(coracle):
     """BASELINE's full size, 5 steps = 2 pairs + 1 single step, bitwise."""
     cfg = W.GridConfig(nx=1581, ny=1301, nz=58)
