@@ -336,7 +336,7 @@ def ghost_rules(U, P, p, g, far_cols=None, far_rows=None):
     return U
 
 
-def _pair_worker(rank, world, port, shape, grid, passes, consts, result_q):
+def _pair_worker(rank, world, port, shape, grid, passes, consts, result_q, pform=False):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -378,8 +378,10 @@ def _pair_worker(rank, world, port, shape, grid, passes, consts, result_q):
             apply_writes(named, rank, allw)
 
         exchange_all({"e": E, "sf": SF, "pb": PB})
-        for _ in range(passes):
-            P = phys(E, SF[:, :, 0], PB[:, :, 0], g)
+        for t in range(passes):
+            # pform: the passes after the first read a post-physics field and all but
+            # the last store one (the library's PIN / POUT); the halos carry it too
+            P = E if pform and t > 0 else phys(E, SF[:, :, 0], PB[:, :, 0], g)
             U1 = ghost_rules(stencil(P, nx, ny, g), P, p, g)    # intermediate on [0, n+1]^2
             P1 = phys(U1, SF[:, :, 0], PB[:, :, 0], g)          # P' (post-physics)
             U2 = np.full_like(E, np.nan)
@@ -395,6 +397,8 @@ def _pair_worker(rank, world, port, shape, grid, passes, consts, result_q):
             far_cols = {"w": allpub[wrap(W_)]["cn"], "e": allpub[wrap(E_)]["c1"]}
             far_rows = {"s": allpub[wrap(S_)]["rn"], "n": allpub[wrap(N_)]["r1"]}
             U2 = ghost_rules(U2, P1, p, g, far_cols, far_rows)
+            if pform and t + 1 < passes:
+                U2 = phys(U2, SF[:, :, 0], PB[:, :, 0], g)
             own = np.full_like(E, np.nan)
             own[li, lj] = U2[li, lj]
             E = own
@@ -413,10 +417,14 @@ def _pair_worker(rank, world, port, shape, grid, passes, consts, result_q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("shape,grid,passes", [
-    ((17, 13, 5), (2, 1), 2), ((17, 13, 5), (1, 2), 2), ((16, 16, 8), (2, 2), 2),
-    ((17, 13, 5), (3, 2), 2), ((33, 29, 11), (2, 4), 1), ((21, 19, 4), (3, 3), 2)])
-def test_decomposed_pair_pass_matches_oracle_bitwise(shape, grid, passes):
+@pytest.mark.parametrize("shape,grid,passes,pform", [
+    ((17, 13, 5), (2, 1), 2, False), ((17, 13, 5), (1, 2), 2, False),
+    ((16, 16, 8), (2, 2), 2, False), ((17, 13, 5), (3, 2), 2, False),
+    ((33, 29, 11), (2, 4), 1, False), ((21, 19, 4), (3, 3), 2, False),
+    # the field kept post-physics between the passes of one call
+    ((17, 13, 5), (2, 1), 3, True), ((16, 16, 8), (2, 2), 3, True),
+    ((21, 19, 4), (3, 3), 2, True)])
+def test_decomposed_pair_pass_matches_oracle_bitwise(shape, grid, passes, pform):
     import torch.multiprocessing as mp
     world = grid[0] * grid[1]
     ctx = mp.get_context("spawn")
@@ -424,7 +432,7 @@ def test_decomposed_pair_pass_matches_oracle_bitwise(shape, grid, passes):
     port = free_port()
     consts = dict(diffusion_velocity=0.125, radiation_intensity=0.37, transfer_velocity=0.013)
     procs = [ctx.Process(target=_pair_worker,
-                         args=(r, world, port, shape, grid, passes, consts, q))
+                         args=(r, world, port, shape, grid, passes, consts, q, pform))
              for r in range(world)]
     for pr in procs:
         pr.start()
