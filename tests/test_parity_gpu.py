@@ -190,6 +190,24 @@ def test_diffusion_sweeps_vs_oracle(coracle, shape, n):
         assert bad.size == 0, (shape, n, f, bad[:5])
 
 
+def test_diffuse_steps_and_reverse_option_errors():
+    """Argument checks of hftw_diffuse_steps and HFTW_OPT_REVERSE (loud, no state change)."""
+    cfg = W.GridConfig(nx=40, ny=30, nz=12)
+    with W.Context(cfg) as ctx:
+        ctx.init()
+        before = ctx.download("energy")
+        with pytest.raises(W.HftwError):
+            ctx.diffuse(-1)
+        with pytest.raises(W.HftwError):
+            ctx.set_option("reverse", 2)
+        ctx.diffuse(0)
+        assert np.array_equal(ctx.download("energy"), before)
+    with W.Context(W.GridConfig(nx=40, ny=30, nz=12), px=2, py=1, devices=[0, 0]) as g:
+        g.init()
+        with pytest.raises(W.HftwError):
+            g.diffuse(3)  # diffusion-only sweeps are single-domain
+
+
 def test_energy_u_observability(coracle):
     """energy_u after a step is the post-physics, pre-diffusion field
     (weather.cpp:118-128 in place, then the swap at :170)."""
