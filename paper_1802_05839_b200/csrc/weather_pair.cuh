@@ -9,7 +9,7 @@
 // (explicitly rounded IEEE ops, the reference's association order), so the
 // result is bitwise identical to two reference steps.
 //
-// Tiling (IJK store, two persistent 320-thread CTAs per SM, dynamic j-major
+// Tiling (IJK store, two persistent 256-thread CTAs per SM, dynamic j-major
 // work units of 30-column strips x 24 rows at ASUCA size, the last ~1.5 waves of
 // units half as tall; 12 / 8-row units on small decomposed domains):
 //   * per row j, ONE TMA box of e_s covers columns i0-2 .. i0+31 and all k,
@@ -18,8 +18,8 @@
 //     strip 0, column 1 for the last strip).  Thread 0 refills the ring slot
 //     a row frees right after the row's barrier (no producer warp);
 //   * row jr of the intermediate P' = physics(e_{s+1}) is computed for the 32
-//     columns i0-1 .. i0+30 from slabs jr-1, jr, jr+1: 10 k-groups of 5-6
-//     planes x 32 columns = 10 warps, each thread walking its planes with a
+//     columns i0-1 .. i0+30 from slabs jr-1, jr, jr+1: 8 k-groups of 7-8
+//     planes x 32 columns = 8 warps, each thread walking its planes with a
 //     register window (k).  P' goes to one of three shared row buffers;
 //   * after a barrier, row j = jr-1 of e_{s+2} is computed for the 30 columns
 //     i0 .. i0+29: the i and j-1 neighbours from the row buffers, the centre,
@@ -60,11 +60,12 @@ constexpr int kPairTX = HFTW_PAIR_TX;           // output columns per strip (30:
 constexpr int kPairIC = kPairTX + 2;            // intermediate columns i0-1 .. i0+TX (warps)
 constexpr int kPairW = kPairTX + 4;             // slab columns i0-2 .. i0+TX+1
 #ifndef HFTW_PAIR_KG
-#define HFTW_PAIR_KG 10
+#define HFTW_PAIR_KG 8
 #endif
-// k-groups (warps) per strip: 10 (<= 6 planes each, 320 threads, 95 registers) ties 8
-// (<= 8 planes, 256 threads, 124 registers; the round-1 layout) at ASUCA size and is 3% faster on the
-// 790 x 325 subdomain of a 2x4 decomposition; 9 / 11 / 12 / 14 are slower
+// k-groups (warps) per strip: 8 (<= 8 planes each, 256 threads, 124 registers).  10
+// groups (<= 6 planes, 320 threads, 95 registers) are 3% faster on a lone 790 x 325
+// subdomain but 0.6% slower at ASUCA size and 1.5% slower on decomposed weak-scaled
+// ranks; 9 / 11 / 12 / 14 are slower still
 constexpr int kPairKG = HFTW_PAIR_KG;
 constexpr int kPairThreads = kPairIC * kPairKG;
 #ifndef HFTW_PAIR_MINB
@@ -577,7 +578,7 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
     // k-groups: planes kl .. kh, nk = kh - kl + 1 <= KPT.  The first and last
     // groups carry the surface / boundary-layer corrections of planes 1 and nz
     // (about one extra plane of work), so the nz % KG extra planes go to the
-    // middle groups first: nz = 58 -> 5 6 6 6 6 6 6 6 6 5 (10 groups).
+    // middle groups first: nz = 58 -> 7 8 8 7 7 7 7 7.
     int kl = 1, nk = 0;
     {
         const int base = nz / kPairKG, rem = nz % kPairKG;
@@ -594,7 +595,7 @@ __global__ void __launch_bounds__(kPairThreads, kPairMinBlocks)
     const bool kfirst = kl == 1, klast = kh == nz;
     // compile-time row shapes: nk in {KPT, KPT-1} x (first, last); else generic
     const int fl = (kfirst ? 1 : 0) + (klast ? 2 : 0);
-    // (an edge group of KPT planes occurs only for nz >= 60, beyond the pair
+    // (an edge group of KPT planes occurs only for nz > 62, beyond the pair
     // kernel's 2-CTA shared-memory budget: it takes the generic path)
     int shape = nz < 2 * kPairKG || fl == 3 ? 16
                 : nk == KPT ? (fl ? 16 : 0) : nk == KPT - 1 ? 4 + fl : 16;

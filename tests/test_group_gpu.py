@@ -48,7 +48,7 @@ def assert_bitwise(got, want, tag):
     ((97, 61, 13), (3, 1), [2, 3], "ijk", "auto"),
     ((100, 70, 9), (3, 2), [3, 2], "ijk", "auto"),
     ((40, 30, 8), (1, 1), [4], "ijk", "auto"),
-    # two-step passes on every rank (AUTO with 50 <= nz <= 58): 2-deep halos,
+    # two-step passes on every rank (AUTO with 56 <= nz <= 58): 2-deep halos,
     # diagonal corner columns, ghost finals from the wrap partners' P'
     ((150, 97, 58), (2, 2), [5, 3], "ijk", "auto"),
     ((140, 90, 51), (2, 2), [6, 4], "ijk", "auto"),

@@ -73,15 +73,15 @@ def test_golden_cases(golden, layout, kernel):
 
 @pytest.mark.parametrize("layout", LAYOUTS)
 def test_auto_kernel_selected(layout):
-    # AUTO: two-step passes (IJK, one domain, 50 <= nz <= 58: the compile-time row
-    # shapes of 10 k-groups of 5-6 planes); the TMA kernel otherwise (fused_pair still
+    # AUTO: two-step passes (IJK, one domain, 56 <= nz <= 58: the compile-time row
+    # shapes of 8 k-groups of 7-8 planes); the TMA kernel otherwise (fused_pair still
     # runs other nz on request)
     with W.Context(W.GridConfig(nx=100, ny=40, nz=58), layout=layout) as ctx:
         assert ctx.kernel == ("fused_pair" if layout == "ijk" else "fused_tma")
         assert ctx.launches_per_step == 1
-    with W.Context(W.GridConfig(nx=100, ny=40, nz=50), layout=layout) as ctx:
+    with W.Context(W.GridConfig(nx=100, ny=40, nz=56), layout=layout) as ctx:
         assert ctx.kernel == ("fused_pair" if layout == "ijk" else "fused_tma")
-    with W.Context(W.GridConfig(nx=100, ny=40, nz=49), layout=layout) as ctx:
+    with W.Context(W.GridConfig(nx=100, ny=40, nz=55), layout=layout) as ctx:
         assert ctx.kernel == "fused_tma"
         if layout == "ijk":
             ctx.set_kernel("fused_pair")
@@ -347,9 +347,9 @@ def test_step_host_after_device_steps(coracle):
 
 @pytest.mark.parametrize("shape", [(100, 37, 58), (64, 64, 2), (65, 3, 9), (2, 2, 2), (33, 200, 17),
                                    (129, 2, 64), (128, 70, 58), (191, 97, 31), (1, 1, 1),
-                                   # k-group splits with compile-time row shapes (10
-                                   # groups of 5-6 planes: nz 50-58), and the first nz
-                                   # past the smem budget
+                                   # k-group splits with compile-time row shapes (8
+                                   # groups of 7-8 planes: nz 56-58), other splits (the
+                                   # generic path), and the first nz past the smem budget
                                    (70, 45, 56), (61, 33, 57), (90, 25, 50), (77, 31, 53),
                                    (64, 40, 55), (95, 20, 59)])
 @pytest.mark.parametrize("steps", [3, 4, 5, 8])
